@@ -1,0 +1,373 @@
+"""Benchmark: fp64 cell-updates/s of steps x (FillBoundary + heat sweep).
+
+Workload: BASELINE.json config 2 (C2) -- periodic 256^3, max_grid_size 64
+(64 boxes of 64^3), 1 ghost, 1 component, tile (1024,8,8), seeded
+Gaussian-plus-noise init, D=1, dt = 0.9*dx^2/6.  A "step" is one
+FillBoundary plus one heat sweep over every box.  Boxes are distributed
+over the ranks by DistributionMapping (strong scaling: total work fixed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Under torchrun each rank drives one GPU; the timed region is bracketed by a
+barrier + cuda synchronize, timed with CUDA events on the launching stream,
+and the max over ranks is reported.  Rank 0 prints one JSON line.
+
+``--impl reference`` times the reference's CPU path (restated in C,
+oracle/tm_oracle.c: tag copies + the four-loop tiled heat kernel, OpenMP
+over all host cores) on rank 0 on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 cell-updates/sec (stencil sweep incl. FillBoundary) and % of HBM roofline"
+UNIT = "cell-updates/s"
+BYTES_PER_CELL = 16  # algorithmic: read u_old + write u_new
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--zmerge", action="store_true", help="fuse z-stacked tiles into one CTA k-march")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-baseline sample length")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def profile_traffic(config_name: str):
+    """dram bytes per sweep launch from the committed ncu capture, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return d.get("heat_sweep", {}).get(config_name, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+            time.sleep(0.15)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference path restated in C (oracle), rank 0 only
+# ---------------------------------------------------------------------------
+def cpu_reference_rate(w, budget_s: float, steps: int | None = None, boxes: int | None = None):
+    """(rate, cores, sample description, steps run, boxes used) for the
+    reference CPU path (tag fill + four-loop tiled heat, all host threads)
+    on the first ``boxes`` boxes of the workload."""
+    import numpy as np
+
+    from oracle import oracle as orc
+    from paper_1604_03570_b200 import BoxArray, Geometry, HeatParams, make_init
+    from paper_1604_03570_b200.box import decompose
+    from paper_1604_03570_b200.fillplan import build_fill_plan_units
+
+    threads = orc.max_threads()
+    ba = BoxArray.chop(w.domain, w.max_grid_size)
+    valids = list(ba)
+    geom = Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    plan = build_fill_plan_units(valids, geom, w.nghost, grids=valids)
+    glob = make_init(w)
+    old = orc.HostMF(valids, w.ncomp, w.nghost)
+    old.from_global(glob)
+    new = orc.HostMF(valids, w.ncomp, w.nghost)
+    c = HeatParams.stable(1.0, geom.dx).coefficients()
+    nb = len(valids) if boxes is None else max(1, min(len(valids), boxes))
+    tags = orc.tags_array([t for t in plan.tags if t.dst_unit < nb])
+    tiles = orc.tiles_array([(u, t) for u in range(nb) for t in decompose(valids[u], w.tile_size)])
+    cells = sum(v.ncells for v in valids[:nb]) * w.ncomp
+    # warm-up pass (page-in, thread pool)
+    orc.fill_boundary(old, tags, threads)
+    orc.heat_step(new, old, tiles, c[:3], c[3], threads)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        orc.fill_boundary(old, tags, threads)
+        orc.heat_step(new, old, tiles, c[:3], c[3], threads)
+        old, new = new, old
+        n += 1
+        el = time.perf_counter() - t0
+        if (steps is not None and n >= steps) or (steps is None and el >= budget_s):
+            break
+    rate = cells * n / el
+    sample = (f"{w.name}: {nb} of {len(valids)} boxes ({cells} cells), {n} x (tag FillBoundary + tiled 4-loop heat), "
+              f"oracle/tm_oracle.c OpenMP x{threads}, {el:.2f} s")
+    return rate, threads, sample, n, nb, el
+
+
+def run_reference(args, w):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    # bound each step: size the per-step sample so the whole run is ~a minute
+    total = max(args.steps + args.warmup, 1)
+    per_step_budget = 60.0 / total
+    probe_rate, _, _, _, _, _ = cpu_reference_rate(w, budget_s=1.0, steps=1, boxes=1)
+    box_cells = w.cells // len(__import__("paper_1604_03570_b200").BoxArray.chop(w.domain, w.max_grid_size))
+    boxes = max(1, int(per_step_budget * probe_rate / box_cells))
+    if args.warmup:
+        cpu_reference_rate(w, 0, steps=args.warmup, boxes=boxes)
+    rate, cores, sample, n, nb, el = cpu_reference_rate(w, 0, steps=args.steps, boxes=boxes)
+    line = {
+        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el / n * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"{w.name}: periodic {w.n}^3, max_grid_size {w.max_grid_size}, nghost {w.nghost}, "
+                               f"ncomp {w.ncomp}, tile {w.tile_size}",
+                   "sample_boxes_per_step": nb},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_ours(args, w):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1604_03570_b200 as tm
+    from paper_1604_03570_b200.runner import HeatRunner
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    glob = tm.make_init(w)
+    glob_pinned = torch.from_numpy(glob).pin_memory()
+    mf = tm.MultiFab(ba, w.ncomp, w.nghost)
+    mf.from_global(glob_pinned.to(dev))
+    params = tm.HeatParams.stable(1.0, geom.dx)
+    plan = tm.build_fill_plan(mf, geom)
+    sched = tm.build_schedule(mf, w.tile_size)
+    runner = HeatRunner(mf, geom, params, sched, plan, use_graph=not args.no_graph, zmerge=args.zmerge)
+    local_cells = sum(ba[u].ncells for u in mf.local_units) * w.ncomp
+    total_cells = w.cells * w.ncomp
+
+    # --- warm-up (includes graph capture) --------------------------------
+    runner.advance(max(args.warmup, 3))
+    barrier()
+
+    # --- timed region: K steps, CUDA events on the launching stream -----
+    stream = torch.cuda.current_stream()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        barrier()
+        ev0.record(stream)
+        runner.advance(args.steps)
+        ev1.record(stream)
+        barrier()
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = total_cells * args.steps / (ms_max * 1e-3)
+
+    # --- dominant kernel: per-launch sweep / fill times (eager, events) --
+    cur = runner.current
+    other = runner.b if cur is runner.a else runner.a
+    nrep = 50
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(3 * nrep)]
+    barrier()
+    for r in range(nrep):
+        evs[3 * r].record(stream)
+        tm.fill_boundary(cur, geom, plan)
+        evs[3 * r + 1].record(stream)
+        tm.heat_step(other, cur, geom, params, sched, zmerge=args.zmerge)
+        evs[3 * r + 2].record(stream)
+        cur, other = other, cur
+    barrier()
+    fill_ms = sum(evs[3 * r].elapsed_time(evs[3 * r + 1]) for r in range(nrep)) / nrep
+    sweep_ms = sum(evs[3 * r + 1].elapsed_time(evs[3 * r + 2]) for r in range(nrep)) / nrep
+    peak, peak_src = peaks()
+    achieved = BYTES_PER_CELL * local_cells / (sweep_ms * 1e-3) / 1e9
+    ghost_cells = sum(t.dst_box.ncells for t in plan.tags if mf.dm[t.dst_unit] == mf.rank) * w.ncomp
+    fill_gbs = 16 * ghost_cells / (fill_ms * 1e-3) / 1e9
+
+    # --- end-to-end through the public API with host buffers -------------
+    # one job = upload phi0 from pinned host memory, run the config's steps
+    # (graph replays), read back the final phi and the checksum.
+    job_steps = w.steps
+    host_out = torch.empty_like(glob_pinned).pin_memory()
+    e2e_runs = 3
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_runs):
+        g = glob_pinned.to(dev, non_blocking=True)
+        runner.a.from_global(g)
+        runner.steps_done = 0
+        out = runner.advance(job_steps)
+        csum = out.reduce_sum_device()
+        host_out.copy_(out.to_global())
+        host_csum = float(csum.item())
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e2e_runs
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    e2e_value = total_cells * job_steps / (e2e_ms * 1e-3)
+    h2d = glob.nbytes
+    d2h = glob.nbytes + 8
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            rate, cores, sample, _, _, _ = cpu_reference_rate(w, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        traffic = profile_traffic(w.name)
+        launches_per_step = 2 + (2 if world > 1 else 0)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"{w.name}: periodic {w.n}^3, max_grid_size {w.max_grid_size} ({len(ba)} boxes), "
+                            f"nghost {w.nghost}, ncomp {w.ncomp}, tile {w.tile_size}, seeded gauss+noise init",
+                "step": "FillBoundary + heat sweep over all boxes",
+                "l2": f"inputs larger than L2: {2 * total_cells * 8 / 1e6:.0f} MB streamed per step vs 126 MB L2",
+                "parallelism": f"dm{world} (contiguous box slabs)", "cuda_graph": runner.use_graph,
+                "zmerge": args.zmerge,
+            },
+            "roofline": {
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": "sweep_kernel<heat> (tm_heat_sweep)",
+                "bytes_per_launch": BYTES_PER_CELL * local_cells, "avg_launch_ms": sweep_ms,
+                "peak_source": peak_src,
+            },
+            "fill": {"avg_launch_ms": fill_ms, "ghost_gbs": fill_gbs, "ghost_cells": ghost_cells,
+                     "share_of_step": fill_ms / (fill_ms + sweep_ms)},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / job_steps,
+                    "d2h_bytes_per_step": d2h / job_steps,
+                    "job": f"upload phi0 (pinned) + {job_steps} steps + download phi + checksum",
+                    "ms_per_job": e2e_ms, "checksum": host_csum},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clocks.summary(),
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    from paper_1604_03570_b200.configs import CONFIGS
+
+    w = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, w)
+    else:
+        run_ours(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,142 @@
+/*
+ * tilemesh_b200.h -- C ABI of libtilemesh_b200.so, the sm_100a kernels
+ * behind the tilemesh stencil-sweep + FillBoundary hot path.
+ *
+ * The reference (/root/reference/pkg/src/tilemesh, Python + numba) has no
+ * C ABI; its replaceable seam is the set of numba loop nests in compiled.py
+ * plus the numpy tag copies of level.py.  Each entry point below replaces
+ * one of them (file:line in the reference):
+ *
+ *   tm_copy_run            level.py:290-294   _run_tags (FillBoundary copies);
+ *                          also halo pack/unpack for remote boxes and the
+ *                          scatter/gather of domain arrays
+ *   tm_heat_sweep          compiled.py:84-99  heat_tiles (flux_x/y/z :32-63
+ *                          + divergence :66-81), driven as kernels.py:174-215
+ *   tm_gsrb_color          (no reference kernel)
+ *   tm_residual_maxnorm    (no reference kernel)
+ *   tm_reduce_sum          level.py:183-190 + compiled.py:20-29 serial_sum
+ *   tm_reduce_minmax       level.py:175-181 reduce_max / reduce_min
+ *
+ * Conventions:
+ *   - every function returns 0 (TM_OK) or a TM_ERR_* code; the message is
+ *     available from tm_last_error() (thread-local); no C++ exceptions
+ *     cross the ABI;
+ *   - device memory is owned by the caller (PyTorch allocations); the
+ *     library only borrows pointers.  Plans are library-owned handles
+ *     holding device copies of their tables;
+ *   - `stream` is a cudaStream_t passed as void*; calls are asynchronous on
+ *     that stream, the caller synchronises;
+ *   - no checks inside kernels (the reference's "unchecked fast path",
+ *     SPEC.md:134); arguments are validated on the host before launch.
+ *
+ * Device storage of a MultiFab ("layout"): one fp64 allocation holding
+ * nslots FAB slots; slot s, component c, plane z, row y, column x lives at
+ *     base[((s*ncomp + c)*nz + z)*ny*pitch + y*pitch + x]
+ * The grown box of a unit sits at slot origin with its first VALID cell at
+ * column xoff (a multiple of 16 doubles = 128 B) and row/plane nghost, so
+ * every valid i-row starts 128-B aligned; pitch is a multiple of 16.
+ */
+#ifndef TILEMESH_B200_H
+#define TILEMESH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TM_OK 0
+#define TM_ERR_INVALID 1 /* bad argument (reference raises ValueError) */
+#define TM_ERR_CUDA 2    /* CUDA runtime / driver failure */
+#define TM_ERR_NOMEM 3
+
+#define TM_ABI_VERSION 1
+
+typedef struct tm_layout {
+    int64_t nslots; /* FAB slots in the allocation */
+    int32_t ncomp;
+    int32_t nghost;
+    int32_t pitch; /* doubles per row, multiple of 16 */
+    int32_t ny;    /* rows per plane  (>= max grown y extent) */
+    int32_t nz;    /* planes per comp (>= max grown z extent) */
+    int32_t xoff;  /* column of the first valid cell, multiple of 16 */
+} tm_layout;
+
+/* One rectangular copy of ex*ey*ez cells x ncomp components.  Offsets are
+ * element offsets of the first cell (component 0) from the side's base. */
+typedef struct tm_copy_tag {
+    int64_t dst_off;
+    int64_t src_off;
+    int32_t ex, ey, ez;
+    int32_t reserved;
+} tm_copy_tag;
+
+/* Addressing of one side of a copy: element strides of y, z and component.
+ * sy == 0 means "packed": the tag's cells are contiguous in x,y,z,c order
+ * (strides ex, ex*ey, ex*ey*ez) -- the halo send/receive buffer format. */
+typedef struct tm_side {
+    int64_t sy, sz, sc;
+} tm_side;
+
+/* One CTA work unit of a sweep: a tile of one FAB slot.  x0,y0,z0 are slot
+ * coordinates of the tile's first cell; parity = (i+j+k)&1 of that cell in
+ * global index space (red/black colouring). */
+typedef struct tm_block {
+    int32_t slot;
+    int32_t x0, y0, z0;
+    int32_t nx, ny, nz;
+    int32_t parity;
+} tm_block;
+
+typedef struct tm_copy_plan tm_copy_plan;
+typedef struct tm_sweep_plan tm_sweep_plan;
+
+const char *tm_last_error(void);
+int tm_abi_version(void);
+/* sm_100a device present and usable (0) or TM_ERR_CUDA */
+int tm_device_check(int device);
+
+/* ---- FillBoundary / halo pack / unpack / scatter / gather ---------------- */
+int tm_copy_plan_create(const tm_copy_tag *tags, int64_t ntags, int32_t ncomp, tm_copy_plan **out);
+int tm_copy_plan_destroy(tm_copy_plan *plan);
+int64_t tm_copy_plan_elements(const tm_copy_plan *plan); /* cells x ncomp */
+int tm_copy_run(const tm_copy_plan *plan, double *dst, const tm_side *dst_side, const double *src,
+                const tm_side *src_side, void *stream);
+
+/* ---- stencil sweeps -------------------------------------------------------- */
+int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan **out);
+int tm_sweep_plan_destroy(tm_sweep_plan *plan);
+
+/* unew = uold + dtD*div(grad uold) on every block cell, components
+ * [comp0, comp0+ncomp_sweep).  Requires uold ghosts (1 layer) filled. */
+int tm_heat_sweep(tm_sweep_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                  int32_t comp0, int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2,
+                  double dtD, void *stream);
+
+/* In-place red (color 0) or black (color 1) Gauss-Seidel update of phi
+ * (component 0) for -lap(phi) = rhs; h2 = dx*dx. */
+int tm_gsrb_color(tm_sweep_plan *plan, const tm_layout *phi_layout, double *phi,
+                  const tm_layout *rhs_layout, const double *rhs, int32_t color, double h2,
+                  void *stream);
+
+/* d_out[0] = max |rhs + (sum6(phi) - 6 phi)/h2| over block cells (device
+ * double, overwritten). */
+int tm_residual_maxnorm(tm_sweep_plan *plan, const tm_layout *phi_layout, const double *phi,
+                        const tm_layout *rhs_layout, const double *rhs, double h2, double *d_out,
+                        void *stream);
+
+/* ---- reductions (one block per unit, blocks in grid order) --------------- */
+/* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =
+ * serial sum of the partials in block order: bit-identical to the
+ * reference reduce_sum. d_partial needs nblocks doubles. */
+int tm_reduce_sum(tm_sweep_plan *plan, const tm_layout *layout, const double *base, int32_t comp,
+                  double *d_partial, double *d_total, void *stream);
+/* d_out[0] = max, d_out[1] = min over block cells of component comp. */
+int tm_reduce_minmax(tm_sweep_plan *plan, const tm_layout *layout, const double *base, int32_t comp,
+                     double *d_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TILEMESH_B200_H */

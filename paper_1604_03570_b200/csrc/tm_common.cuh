@@ -1,0 +1,91 @@
+// Shared helpers for the sm_100a kernels: error plumbing for the C ABI,
+// layout arithmetic, and the mbarrier / TMA (cp.async.bulk.tensor) PTX
+// wrappers used to stage stencil planes into shared memory.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "tilemesh_b200.h"
+
+namespace tmk {
+
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// element strides of a layout
+struct Strides {
+    int64_t row, plane, comp, slot;
+};
+inline __host__ __device__ Strides strides_of(const tm_layout &L) {
+    Strides s;
+    s.row = L.pitch;
+    s.plane = (int64_t)L.pitch * L.ny;
+    s.comp = s.plane * L.nz;
+    s.slot = s.comp * L.ncomp;
+    return s;
+}
+
+int check_layout(const tm_layout *L, const char *who);
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
+int encode_plane_map(CUtensorMap *map, const tm_layout &L, const double *base, int box_x, int box_y);
+
+// ---------------------------------------------------------------- device PTX
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "TM_WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra TM_WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// 4-D tiled TMA load (x, y, z, slot*ncomp+comp) into shared memory, completion
+// signalled on `bar` as transaction bytes.
+__device__ __forceinline__ void tma_load_plane(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y,
+                                               int z, int w) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "r"(w)
+        : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tensormap(const CUtensorMap *map) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+// IEEE round-to-nearest binary64 ops that the compiler may not contract
+// into FMA: the reference arithmetic is FMA-free.
+__device__ __forceinline__ double rn_sub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double rn_add(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double rn_mul(double a, double b) { return __dmul_rn(a, b); }
+
+}  // namespace tmk

@@ -1,0 +1,120 @@
+"""Inter-GPU FillBoundary: packed halo messages over NCCL.
+
+The reference is single-process and has no exchange; the
+multi-GPU path is new.  Each rank holds the global
+FillBoundary plan (identical on every rank: it is a pure function of the
+BoxArray, geometry and ghost width) and the DistributionMapping, so both
+ends of every message derive the same layout without any metadata
+exchange:
+
+* the message from rank a to rank b is the ordered list of plan tags whose
+  source unit a owns and whose destination unit b owns, each tag's cells
+  packed x-fastest then y, z, component (``tm_side`` "packed" format);
+* rank a packs all its outgoing messages with one copy-kernel launch into
+  one send buffer, the messages go out as one grouped NCCL send/recv
+  (``torch.distributed.batch_isend_irecv``), and rank b unpacks all its
+  incoming messages with one launch straight into ghost cells.
+
+Intra-rank tags never touch a buffer: they are the local copy kernel.
+"""
+
+from __future__ import annotations
+
+from collections import OrderedDict
+
+import numpy as np
+
+from . import _native
+
+
+def exchange_lists(owners, tags, me: int):
+    """Split plan tag indices for rank ``me``:
+    ``(local, sends{peer: [tag ids]}, recvs{peer: [tag ids]})``; peers in
+    ascending rank order, tag ids in plan order on both ends."""
+    local = []
+    sends: dict = {}
+    recvs: dict = {}
+    for n, t in enumerate(tags):
+        so, do = owners[t[2]], owners[t[0]]
+        if so == me and do == me:
+            local.append(n)
+        elif so == me:
+            sends.setdefault(do, []).append(n)
+        elif do == me:
+            recvs.setdefault(so, []).append(n)
+    return (local, OrderedDict(sorted(sends.items())), OrderedDict(sorted(recvs.items())))
+
+
+def tag_elements(tag, ncomp: int) -> int:
+    e = tag[1].extents
+    return e[0] * e[1] * e[2] * ncomp
+
+
+class HaloExchange:
+    """Pack / grouped send-recv / unpack for one (MultiFab layout, plan)."""
+
+    def __init__(self, mf, plan):
+        import torch
+
+        from .multifab import cell_offsets
+
+        self.mf = mf
+        tags = plan.tags
+        _, sends, recvs = exchange_lists(mf.dm.owners, tags, mf.rank)
+        nc = mf.ncomp
+
+        def build(groups, remote_side_is_dst):
+            rows = []
+            spans = []
+            off = 0
+            for peer, ids in groups.items():
+                start = off
+                for n in ids:
+                    t = tags[n]
+                    e = t[1].extents
+                    rows.append((t, off, e))
+                    off += e[0] * e[1] * e[2] * nc
+                spans.append((peer, start, off - start))
+            arr = np.zeros(len(rows), dtype=_native.COPY_TAG_DTYPE)
+            if rows:
+                units = np.array([r[0][2] if remote_side_is_dst else r[0][0] for r in rows], dtype=np.int64)
+                cells = np.array([r[0][3].lo if remote_side_is_dst else r[0][1].lo for r in rows], dtype=np.int64)
+                field = cell_offsets(mf, units, cells)
+                buf = np.array([r[1] for r in rows], dtype=np.int64)
+                ext = np.array([r[2] for r in rows], dtype=np.int64)
+                if remote_side_is_dst:  # pack: storage -> send buffer
+                    arr["dst_off"], arr["src_off"] = buf, field
+                else:  # unpack: receive buffer -> storage
+                    arr["dst_off"], arr["src_off"] = field, buf
+                arr["ex"], arr["ey"], arr["ez"] = ext[:, 0], ext[:, 1], ext[:, 2]
+            return arr, spans, off
+
+        pack_tags, self.send_spans, nsend = build(sends, True)
+        unpack_tags, self.recv_spans, nrecv = build(recvs, False)
+        self.pack = _native.CopyPlan(pack_tags, nc)
+        self.unpack = _native.CopyPlan(unpack_tags, nc)
+        self.sendbuf = torch.empty(max(nsend, 1), dtype=torch.float64, device=mf.device)
+        self.recvbuf = torch.empty(max(nrecv, 1), dtype=torch.float64, device=mf.device)
+        self.bytes_sent = nsend * 8
+        self.bytes_recv = nrecv * 8
+        self._reqs = None
+
+    def start(self, stream: int) -> None:
+        import torch.distributed as dist
+
+        mf = self.mf
+        packed = (0, 0, 0)
+        self.pack.run(self.sendbuf.data_ptr(), packed, mf.ptr, mf.layout.side(), stream)
+        ops = []
+        for peer, off, n in self.send_spans:
+            ops.append(dist.P2POp(dist.isend, self.sendbuf[off:off + n], peer))
+        for peer, off, n in self.recv_spans:
+            ops.append(dist.P2POp(dist.irecv, self.recvbuf[off:off + n], peer))
+        self._reqs = dist.batch_isend_irecv(ops) if ops else []
+
+    def finish(self, stream: int) -> None:
+        for r in self._reqs or []:
+            r.wait()
+        self._reqs = None
+        mf = self.mf
+        self.unpack.run(mf.ptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)

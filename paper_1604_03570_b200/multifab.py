@@ -1,0 +1,579 @@
+"""Device-resident MultiFab and FillBoundary.
+
+Reference: ``MultiFab`` (level.py:102-190), ``FArrayBox`` (fab.py:19-97),
+``fill_boundary`` (level.py:297-323).
+
+Storage (north star item 1): every MultiFab owns ONE
+fp64 allocation of shape ``(nslots, ncomp, nz, ny, pitch)`` on its GPU, one
+slot per unit this rank owns.  A unit's grown box sits at the slot origin
+with its first valid cell at column ``xoff`` (a multiple of 16 doubles), so
+every valid i-row starts on a 128-B boundary, and ``pitch`` is a multiple
+of 16 doubles.  Within a slot the order is the reference's: x fastest, then
+y, z, component slowest.  Uniform slots let one TMA tensor map describe the
+whole MultiFab (dims x, y, z, slot*ncomp).
+
+PyTorch is only the allocator here; every data-path operation is a kernel
+of ``libtilemesh_b200.so`` launched on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import warnings
+from typing import Callable, NamedTuple
+
+import numpy as np
+
+from . import _native
+from .box import Box, decompose, grow, split_extent
+from .boxarray import BoxArray, DistributionMapping, Geometry
+from .fillplan import FillPlan, build_fill_plan
+from .mfiter import TileSchedule, build_schedule
+
+CONTIGUOUS = "contiguous"
+REGIONAL = "regional"
+ROW_ALIGN = 16  # doubles: 128 B
+
+# CTA tile limits of the sweep kernels (tm_stencil.cu): a block must fit the
+# TMA box (nx + 2 <= 256) and at most 64 warp-row segments of 32 cells.
+MAX_BLOCK_NX = 128
+MAX_BLOCK_SEGS = 64
+
+
+def _round_up(v: int, m: int) -> int:
+    return -(-v // m) * m
+
+
+def comm_info():
+    """(rank, world_size) of the default torch.distributed group, or (0, 1)."""
+    try:
+        import torch.distributed as dist
+
+        if dist.is_available() and dist.is_initialized():
+            return dist.get_rank(), dist.get_world_size()
+    except ImportError:  # pragma: no cover
+        pass
+    return 0, 1
+
+
+class StorageLayout(NamedTuple):
+    nslots: int
+    ncomp: int
+    nghost: int
+    pitch: int
+    ny: int
+    nz: int
+    xoff: int
+
+    @staticmethod
+    def for_units(valids, ncomp: int, nghost: int) -> "StorageLayout":
+        if valids:
+            mx = max(v.extents[0] for v in valids)
+            my = max(v.extents[1] for v in valids)
+            mz = max(v.extents[2] for v in valids)
+        else:
+            mx = my = mz = 1
+        xoff = _round_up(nghost, ROW_ALIGN)
+        pitch = _round_up(xoff + mx + nghost, ROW_ALIGN)
+        return StorageLayout(len(valids), ncomp, nghost, pitch, my + 2 * nghost, mz + 2 * nghost, xoff)
+
+    @property
+    def row(self) -> int:
+        return self.pitch
+
+    @property
+    def plane(self) -> int:
+        return self.pitch * self.ny
+
+    @property
+    def comp(self) -> int:
+        return self.plane * self.nz
+
+    @property
+    def slot(self) -> int:
+        return self.comp * self.ncomp
+
+    def side(self) -> tuple:
+        return (self.row, self.plane, self.comp)
+
+    def to_c(self) -> "_native.tm_layout":
+        return _native.tm_layout(*self)
+
+
+class Unit(NamedTuple):
+    grid: int
+    valid: Box
+    fab: "DeviceFab | None"  # None for units owned by another rank
+
+
+class DeviceFab:
+    """One unit's FAB: a view of its slot in the MultiFab allocation.
+
+    ``data`` is indexed like the reference's ``FArrayBox.data``:
+    ``data[i - lo0, j - lo1, k - lo2, c]`` over the allocation (grown) box.
+    """
+
+    def __init__(self, mf: "MultiFab", slot: int, abox: Box):
+        self.abox = abox
+        self.ncomp = mf.ncomp
+        self.slot = slot
+        L = mf.layout
+        nx, ny, nz = abox.extents
+        x0 = L.xoff - mf.nghost
+        blk = mf.data[slot, :, :nz, :ny, x0:x0 + nx]  # (c, z, y, x)
+        self.data = blk.permute(3, 2, 1, 0)  # (x, y, z, c)
+
+    def _check(self, i, j, k, c):
+        if not self.abox.contains_point((i, j, k)):
+            raise IndexError(f"index ({i},{j},{k}) outside {self.abox}")
+        if not 0 <= c < self.ncomp:
+            raise IndexError(f"component {c} out of range [0,{self.ncomp})")
+
+    def at(self, i: int, j: int, k: int, c: int = 0) -> float:
+        self._check(i, j, k, c)
+        lo = self.abox.lo
+        return float(self.data[i - lo[0], j - lo[1], k - lo[2], c].item())
+
+    def set_at(self, i: int, j: int, k: int, v: float, c: int = 0) -> None:
+        self._check(i, j, k, c)
+        lo = self.abox.lo
+        self.data[i - lo[0], j - lo[1], k - lo[2], c] = v
+
+    def view(self, region: Box, c0: int = 0, nc: int | None = None):
+        if not self.abox.contains(region):
+            raise ValueError(f"region {region} not contained in {self.abox}")
+        if nc is None:
+            nc = self.ncomp - c0
+        if c0 < 0 or c0 + nc > self.ncomp:
+            raise ValueError(f"components [{c0},{c0 + nc}) out of range")
+        lo = self.abox.lo
+        sl = tuple(slice(region.lo[d] - lo[d], region.hi[d] - lo[d] + 1) for d in range(3))
+        return self.data[sl + (slice(c0, c0 + nc),)]
+
+    def comp(self, c: int = 0):
+        return self.data[:, :, :, c]
+
+    def fill(self, v: float, region: Box | None = None, c: int | None = None) -> None:
+        region = self.abox if region is None else region
+        if c is None:
+            self.view(region).fill_(v)
+        else:
+            self.view(region, c, 1).fill_(v)
+
+    def to_numpy(self) -> np.ndarray:
+        """Host copy in the reference layout: (nx, ny, nz, ncomp), F-order."""
+        return np.asfortranarray(self.data.cpu().numpy())
+
+
+class MultiFab:
+    """Device MultiFab with the reference constructor signature.
+
+    ``dm`` (DistributionMapping over grids) selects the units this rank
+    stores; by default grids are partitioned over the ranks of the default
+    torch.distributed group (one rank when it is not initialised).
+    """
+
+    def __init__(self, ba: BoxArray, ncomp: int = 1, nghost: int = 0, layout: str = CONTIGUOUS,
+                 region_size=None, zero: bool = True, dm: DistributionMapping | None = None,
+                 device=None, rank: int | None = None):
+        import torch
+
+        if nghost < 0:
+            raise ValueError(f"nghost must be non-negative, got {nghost}")
+        if ncomp < 1:
+            raise ValueError(f"ncomp must be positive, got {ncomp}")
+        if layout not in (CONTIGUOUS, REGIONAL):
+            raise ValueError(f"unknown layout {layout!r}")
+        if layout == REGIONAL:
+            if region_size is None:
+                raise ValueError("regional layout requires a region_size")
+            raise NotImplementedError("regional layout is not on the device path yet (DESIGN.md §7)")
+        if not torch.cuda.is_available():
+            raise _native.TilemeshError("tilemesh_b200 MultiFab needs a CUDA device (no CPU fallback)")
+        self.ba = ba
+        self.ncomp = ncomp
+        self.nghost = nghost
+        self.layout_kind = layout
+        self.region_size = region_size
+        crank, cworld = comm_info()
+        if dm is None:
+            dm = DistributionMapping(ba, cworld)
+        self.dm = dm
+        self.rank = crank if rank is None else rank
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        valids = list(ba)
+        self.local_units = [u for u in range(len(valids)) if dm[u] == self.rank]
+        self.slot_of = {u: s for s, u in enumerate(self.local_units)}
+        self.layout = StorageLayout.for_units([valids[u] for u in self.local_units], ncomp, nghost)
+        L = self.layout
+        shape = (L.nslots, ncomp, L.nz, L.ny, L.pitch)
+        alloc = torch.zeros if zero else torch.empty
+        self.data = alloc(shape, dtype=torch.float64, device=self.device)
+        self.units = []
+        for u, v in enumerate(valids):
+            fab = None
+            if u in self.slot_of:
+                fab = DeviceFab(self, self.slot_of[u], grow(v, nghost) if nghost > 0 else v)
+            self.units.append(Unit(u, v, fab))
+        self._plans: dict = {}
+        self._unit_sweep = None
+        self._scratch = {}
+
+    # ------------------------------------------------------------------ misc
+    def clone_empty(self) -> "MultiFab":
+        """Same layout and distribution, uninitialised storage (level.py:135-138)."""
+        return MultiFab(self.ba, self.ncomp, self.nghost, self.layout_kind, self.region_size, zero=False,
+                        dm=self.dm, device=self.device, rank=self.rank)
+
+    def fab(self, u: int) -> DeviceFab:
+        f = self.units[u].fab
+        if f is None:
+            raise KeyError(f"unit {u} is owned by rank {self.dm[u]}, not {self.rank}")
+        return f
+
+    def __getitem__(self, mfi) -> DeviceFab:
+        return self.fab(mfi.index() if hasattr(mfi, "index") else int(mfi))
+
+    @property
+    def ptr(self) -> int:
+        return self.data.data_ptr()
+
+    def stream(self) -> int:
+        return _native.stream_handle(self.device)
+
+    def same_layout(self, other: "MultiFab") -> bool:
+        return self.layout == other.layout and self.local_units == other.local_units and self.ba == other.ba
+
+    # ----------------------------------------------------- host <-> device I/O
+    def set_from_function(self, fn: Callable, comp: int = 0) -> None:
+        """Valid cells of one component from ``fn(i, j, k)`` evaluated on the host."""
+        import torch
+
+        for u in self.local_units:
+            v = self.units[u].valid
+            I, J, K = np.ogrid[v.lo[0]:v.hi[0] + 1, v.lo[1]:v.hi[1] + 1, v.lo[2]:v.hi[2] + 1]
+            vals = np.broadcast_to(np.asarray(fn(I, J, K), dtype=np.float64), v.extents)
+            self.fab(u).view(v, comp, 1)[..., 0].copy_(torch.from_numpy(np.ascontiguousarray(vals)))
+
+    def fill(self, v: float, comp: int | None = None) -> None:
+        if comp is None:
+            self.data.fill_(v)
+        else:
+            self.data[:, comp].fill_(v)
+
+    def _global_copy_plan(self, domain: Box, direction: str):
+        key = ("global", direction, domain)
+        plan = self._plans.get(key)
+        if plan is None:
+            n = domain.extents
+            gs = (n[0], n[0] * n[1], n[0] * n[1] * n[2])
+            L = self.layout
+            tags = np.zeros(len(self.local_units), dtype=_native.COPY_TAG_DTYPE)
+            for t, u in enumerate(self.local_units):
+                v = self.units[u].valid
+                e = v.extents
+                g_off = (v.lo[0] - domain.lo[0]) + gs[0] * (v.lo[1] - domain.lo[1]) + gs[1] * (v.lo[2] - domain.lo[2])
+                m_off = self.slot_of[u] * L.slot + L.nghost * L.plane + L.nghost * L.row + L.xoff
+                if direction == "scatter":
+                    tags[t] = (m_off, g_off, e[0], e[1], e[2], 0)
+                else:
+                    tags[t] = (g_off, m_off, e[0], e[1], e[2], 0)
+            plan = (_native.CopyPlan(tags, self.ncomp), gs)
+            self._plans[key] = plan
+        return plan
+
+    def from_global(self, glob, domain: Box | None = None) -> None:
+        """Valid cells from a domain-shaped array ``(ncomp, nz, ny, nx)``
+        (numpy on the host, or a torch tensor on this device)."""
+        import torch
+
+        domain = self.ba_domain() if domain is None else domain
+        if isinstance(glob, np.ndarray):
+            g = torch.from_numpy(np.ascontiguousarray(glob, dtype=np.float64)).to(self.device, non_blocking=True)
+        else:
+            g = glob.to(self.device, dtype=torch.float64).contiguous()
+        n = domain.extents
+        if tuple(g.shape) != (self.ncomp, n[2], n[1], n[0]):
+            raise ValueError(f"global array shape {tuple(g.shape)} != {(self.ncomp, n[2], n[1], n[0])}")
+        plan, gs = self._global_copy_plan(domain, "scatter")
+        plan.run(self.ptr, self.layout.side(), g.data_ptr(), gs, self.stream())
+        self._keepalive = g
+
+    def to_global(self, domain: Box | None = None, out=None):
+        """Valid cells of the units this rank owns gathered into a device
+        tensor ``(ncomp, nz, ny, nx)`` (cells of other ranks' units stay 0)."""
+        import torch
+
+        domain = self.ba_domain() if domain is None else domain
+        n = domain.extents
+        if out is None:
+            out = torch.zeros((self.ncomp, n[2], n[1], n[0]), dtype=torch.float64, device=self.device)
+        plan, gs = self._global_copy_plan(domain, "gather")
+        plan.run(out.data_ptr(), gs, self.ptr, self.layout.side(), self.stream())
+        return out
+
+    def ba_domain(self) -> Box:
+        from .box import bounding_box
+
+        return bounding_box(self.ba)
+
+    def grid_valid_array(self, g: int, comp: int = 0) -> np.ndarray:
+        """Valid data of grid ``g`` as a host ``(nx, ny, nz)`` array (level.py:152-167)."""
+        u = self.units[g]
+        return np.asfortranarray(self.fab(g).view(u.valid, comp, 1)[..., 0].cpu().numpy())
+
+    # -------------------------------------------------------------- reductions
+    def _check_reduce(self, comp: int) -> None:
+        if len(self.ba) == 0:
+            raise ValueError("reduction over an empty BoxArray")
+        if not 0 <= comp < self.ncomp:
+            raise ValueError(f"component {comp} out of range")
+
+    def unit_sweep_plan(self) -> "_native.SweepPlan":
+        """One block per local unit covering its valid box, in unit order."""
+        if self._unit_sweep is None:
+            L = self.layout
+            b = np.zeros(len(self.local_units), dtype=_native.BLOCK_DTYPE)
+            for n, u in enumerate(self.local_units):
+                v = self.units[u].valid
+                e = v.extents
+                b[n] = (self.slot_of[u], L.xoff, L.nghost, L.nghost, e[0], e[1], e[2], sum(v.lo) & 1)
+            self._unit_sweep = _native.SweepPlan(b)
+        return self._unit_sweep
+
+    def _scratch_buf(self, name: str, n: int):
+        import torch
+
+        buf = self._scratch.get(name)
+        if buf is None or buf.numel() < n:
+            buf = torch.empty(max(n, 2), dtype=torch.float64, device=self.device)
+            self._scratch[name] = buf
+        return buf
+
+    def reduce_sum_device(self, comp: int = 0):
+        """Checksum on the device: a 1-element tensor, bit-identical to the
+        reference ``reduce_sum`` (grid order, serial x-fastest per grid)."""
+        import torch
+
+        self._check_reduce(comp)
+        rank, world = comm_info()
+        nunits = len(self.units)
+        L = _native.load()
+        plan = self.unit_sweep_plan()
+        if world == 1 or len(self.local_units) == nunits:
+            part = self._scratch_buf("partial", max(nunits, 1))
+            tot = self._scratch_buf("total", 2)
+            _native.check(L.tm_reduce_sum(plan.handle, self.layout.to_c(), self.ptr, comp, part.data_ptr(),
+                                          tot.data_ptr(), self.stream()), "tm_reduce_sum")
+            return tot[:1]
+        import torch.distributed as dist
+
+        part = self._scratch_buf("partial", max(len(self.local_units), 1))
+        tot = self._scratch_buf("total", 2)
+        if self.local_units:
+            _native.check(L.tm_reduce_sum(plan.handle, self.layout.to_c(), self.ptr, comp, part.data_ptr(),
+                                          tot.data_ptr(), self.stream()), "tm_reduce_sum")
+        full = torch.zeros(nunits, dtype=torch.float64, device=self.device)
+        idx = torch.as_tensor(self.local_units, dtype=torch.long, device=self.device)
+        full.index_copy_(0, idx, part[:len(self.local_units)])
+        dist.all_reduce(full)  # each entry has exactly one non-zero contributor: exact
+        # grid partials combined serially in grid order (nunits scalars)
+        total = 0.0
+        for v in full.cpu().tolist():
+            total += v
+        return torch.tensor([total], dtype=torch.float64, device=self.device)
+
+    def reduce_sum(self, comp: int = 0) -> float:
+        return float(self.reduce_sum_device(comp).item())
+
+    def _minmax(self, comp: int):
+        import torch
+
+        self._check_reduce(comp)
+        out = self._scratch_buf("minmax", 2)
+        L = _native.load()
+        rank, world = comm_info()
+        if self.local_units:
+            _native.check(L.tm_reduce_minmax(self.unit_sweep_plan().handle, self.layout.to_c(), self.ptr, comp,
+                                             out.data_ptr(), self.stream()), "tm_reduce_minmax")
+        else:
+            out[0] = -float("inf")
+            out[1] = float("inf")
+        if world > 1:
+            import torch.distributed as dist
+
+            mx = out[:1].clone()
+            mn = out[1:2].clone()
+            dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+            dist.all_reduce(mn, op=dist.ReduceOp.MIN)
+            return float(mx.item()), float(mn.item())
+        o = out[:2].cpu()
+        return float(o[0]), float(o[1])
+
+    def reduce_max(self, comp: int = 0) -> float:
+        return self._minmax(comp)[0]
+
+    def reduce_min(self, comp: int = 0) -> float:
+        return self._minmax(comp)[1]
+
+
+def build_multifab(ba, ncomp=1, nghost=0, layout=CONTIGUOUS, region_size=None, **kw):
+    return MultiFab(ba, ncomp, nghost, layout, region_size, **kw)
+
+
+# --------------------------------------------------------------------------
+# device tables
+# --------------------------------------------------------------------------
+def _tag_arrays(tags):
+    n = len(tags)
+    du = np.empty(n, dtype=np.int64)
+    su = np.empty(n, dtype=np.int64)
+    dlo = np.empty((n, 3), dtype=np.int64)
+    slo = np.empty((n, 3), dtype=np.int64)
+    ext = np.empty((n, 3), dtype=np.int64)
+    for t, g in enumerate(tags):
+        du[t] = g[0]
+        su[t] = g[2]
+        dlo[t] = g[1].lo
+        slo[t] = g[3].lo
+        ext[t] = g[1].extents
+    return du, dlo, su, slo, ext
+
+
+def cell_offsets(mf: MultiFab, units: np.ndarray, cells: np.ndarray) -> np.ndarray:
+    """Element offsets in ``mf.data`` of global cells ``cells`` (n, 3) of
+    units ``units`` (component 0)."""
+    L = mf.layout
+    vlo = np.array([mf.units[u].valid.lo for u in range(len(mf.units))], dtype=np.int64).reshape(-1, 3)
+    slot = np.full(len(mf.units), -1, dtype=np.int64)
+    for u, s in mf.slot_of.items():
+        slot[u] = s
+    s = slot[units]
+    if np.any(s < 0):
+        raise ValueError("cell offsets requested for a unit this rank does not own")
+    rel = cells - vlo[units]
+    return (s * L.slot + (rel[:, 2] + L.nghost) * L.plane + (rel[:, 1] + L.nghost) * L.row
+            + (rel[:, 0] + L.xoff))
+
+
+def local_copy_tags(mf: MultiFab, tags) -> np.ndarray:
+    """FillBoundary tags whose source and destination units both live on
+    this rank, as device copy tags (both sides in ``mf.data``)."""
+    if not tags:
+        return np.zeros(0, dtype=_native.COPY_TAG_DTYPE)
+    du, dlo, su, slo, ext = _tag_arrays(tags)
+    out = np.zeros(len(tags), dtype=_native.COPY_TAG_DTYPE)
+    out["dst_off"] = cell_offsets(mf, du, dlo)
+    out["src_off"] = cell_offsets(mf, su, slo)
+    out["ex"], out["ey"], out["ez"] = ext[:, 0], ext[:, 1], ext[:, 2]
+    return out
+
+
+def _plan_key(mf: MultiFab):
+    return (mf.layout, tuple(mf.local_units), mf.rank, mf.dm.nranks, mf.ncomp)
+
+
+def _device_fill(mf: MultiFab, plan: FillPlan):
+    key = _plan_key(mf)
+    dev = plan._device.get(key)
+    if dev is None:
+        from .halo import HaloExchange
+
+        owners = mf.dm.owners
+        local = [t for t in plan.tags if owners[t.dst_unit] == mf.rank and owners[t.src_unit] == mf.rank]
+        copy = _native.CopyPlan(local_copy_tags(mf, local), mf.ncomp)
+        halo = HaloExchange(mf, plan) if mf.dm.nranks > 1 else None
+        dev = (copy, halo)
+        plan._device[key] = dev
+    return dev
+
+
+def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, workers: int = 1) -> None:
+    """Copy valid data into every fillable ghost cell (level.py:297-323).
+
+    Intra-GPU tags run as one packed copy kernel; tags whose source box is
+    on another rank travel as packed halo messages (``halo.HaloExchange``).
+    ``workers`` is accepted for API parity and ignored (the kernel is the
+    parallelism).
+    """
+    if plan is None:
+        plan = mf._plans.get(("fill", geom))
+        if plan is None:
+            plan = build_fill_plan(mf, geom)
+            mf._plans[("fill", geom)] = plan
+    copy, halo = _device_fill(mf, plan)
+    stream = mf.stream()
+    if halo is not None:
+        halo.start(stream)
+    copy.run(mf.ptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
+    if halo is not None:
+        halo.finish(stream)
+
+
+FillBoundary = fill_boundary
+
+
+# --------------------------------------------------------------------------
+# sweep blocks from tile schedules
+# --------------------------------------------------------------------------
+def split_tile(tile: Box) -> list:
+    """Cut a schedule tile into CTA-sized blocks (x <= 128, <= 64 row
+    segments).  The stencil results do not depend on the cut."""
+    e = tile.extents
+    xs = split_extent(tile.lo[0], e[0], MAX_BLOCK_NX) if e[0] > MAX_BLOCK_NX else [(tile.lo[0], tile.hi[0])]
+    out = []
+    for (x0, x1) in xs:
+        segs = -(-(x1 - x0 + 1) // 32)
+        max_rows = max(1, MAX_BLOCK_SEGS // segs)
+        ys = split_extent(tile.lo[1], e[1], max_rows) if e[1] > max_rows else [(tile.lo[1], tile.hi[1])]
+        for (y0, y1) in ys:
+            out.append(Box((x0, y0, tile.lo[2]), (x1, y1, tile.hi[2])))
+    return out
+
+
+def sweep_blocks(mf: MultiFab, entries, zmerge: bool = False) -> np.ndarray:
+    """Device block table for (unit, tile) entries of this rank's units."""
+    L = mf.layout
+    rows = []
+    for unit, tile in entries:
+        if unit not in mf.slot_of:
+            continue
+        v = mf.units[unit].valid
+        s = mf.slot_of[unit]
+        for b in split_tile(tile):
+            e = b.extents
+            rows.append((s, L.xoff + b.lo[0] - v.lo[0], L.nghost + b.lo[1] - v.lo[1],
+                         L.nghost + b.lo[2] - v.lo[2], e[0], e[1], e[2], (b.lo[0] + b.lo[1] + b.lo[2]) & 1))
+    arr = np.array(rows, dtype=np.int64).reshape(-1, 8)
+    if zmerge and len(arr):
+        arr = merge_z(arr)
+    out = np.zeros(len(arr), dtype=_native.BLOCK_DTYPE)
+    for n, name in enumerate(_native.BLOCK_DTYPE.names):
+        out[name] = arr[:, n]
+    return out
+
+
+def merge_z(arr: np.ndarray) -> np.ndarray:
+    """Fuse blocks stacked in z over the same (slot, x, y) footprint into one
+    longer k-march (bit-identical results, fewer halo planes re-read)."""
+    order = np.lexsort((arr[:, 3], arr[:, 5], arr[:, 4], arr[:, 2], arr[:, 1], arr[:, 0]))
+    a = arr[order]
+    merged = []
+    cur = a[0].copy()
+    for r in a[1:]:
+        if (r[0] == cur[0] and r[1] == cur[1] and r[2] == cur[2] and r[4] == cur[4] and r[5] == cur[5]
+                and r[3] == cur[3] + cur[6]):
+            cur[6] += r[6]
+        else:
+            merged.append(cur)
+            cur = r.copy()
+    merged.append(cur)
+    return np.array(merged, dtype=np.int64)
+
+
+def schedule_sweep_plan(mf: MultiFab, schedule: TileSchedule, zmerge: bool = False) -> "_native.SweepPlan":
+    key = (mf.layout, tuple(mf.local_units), zmerge)
+    plan = schedule._device.get(key)
+    if plan is None:
+        plan = _native.SweepPlan(sweep_blocks(mf, schedule.entries, zmerge))
+        schedule._device[key] = plan
+    return plan

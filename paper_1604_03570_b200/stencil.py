@@ -1,0 +1,178 @@
+"""Stencil drivers: forward-Euler heat, red-black Gauss-Seidel, residual.
+
+Reference: ``HeatParams`` (kernels.py:26-46), ``heat_step``
+(kernels.py:174-215).  GSRB and the residual max-norm have no reference
+(SURVEY.md §8a a12/a13); their canonical per-cell forms are fixed here and
+in ``oracle/tm_oracle.c``.
+
+Each driver validates on the host (``ValueError`` before any kernel runs,
+as the reference does) and then issues ONE kernel launch covering every
+tile of every box this rank owns, on the current torch stream.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+from . import _native
+from .boxarray import Geometry
+from .mfiter import TileSchedule, build_schedule
+from .multifab import MultiFab, schedule_sweep_plan
+
+
+@dataclass(frozen=True)
+class HeatParams:
+    diffusivity: float
+    dt: float
+    dx: tuple
+
+    def __post_init__(self):
+        if self.diffusivity <= 0 or self.dt <= 0 or any(d <= 0 for d in self.dx):
+            raise ValueError("diffusivity, dt and dx must all be positive")
+
+    @property
+    def stability_limit(self) -> float:
+        return 1.0 / (2.0 * self.diffusivity * sum(1.0 / d ** 2 for d in self.dx))
+
+    @staticmethod
+    def stable(diffusivity: float, dx, safety: float = 0.9) -> "HeatParams":
+        """dt = safety x forward-Euler bound (same expression as the reference,
+        so dt is bit-identical)."""
+        if isinstance(dx, (int, float)):
+            dx = (float(dx),) * 3
+        limit = 1.0 / (2.0 * diffusivity * sum(1.0 / d ** 2 for d in dx))
+        return HeatParams(diffusivity, safety * limit, tuple(dx))
+
+    def coefficients(self) -> tuple:
+        """(dxi0, dxi1, dxi2, dtD) computed as kernels.py:196-197 does."""
+        dxi = tuple(1.0 / d for d in self.dx)
+        return dxi + (self.diffusivity * self.dt,)
+
+
+def _schedule_for(mf: MultiFab, schedule):
+    if schedule is None:
+        return build_schedule(mf, "off")
+    if not isinstance(schedule, TileSchedule):
+        return build_schedule(mf, schedule)
+    return schedule
+
+
+def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatParams,
+              schedule: TileSchedule | None = None, workers: int = 1, arenas=None, verify: bool = False,
+              zmerge: bool = False) -> None:
+    """One forward-Euler step on every valid cell of every component; the
+    ghosts of ``mf_old`` must have been filled (FillBoundary) beforehand.
+
+    ``u_new`` is written on valid cells only; its ghosts are untouched
+    (double buffering, reference kernels.py:4-7).  ``workers``/``arenas``
+    are accepted for API parity: tile parallelism is the CTA grid and flux
+    scratch lives in registers.  Unlike the reference (ncomp == 1 only,
+    kernels.py:147-150) every component is updated, which is what config C3
+    needs.
+    """
+    if mf_old.nghost < 1:
+        raise ValueError("heat kernel requires nghost >= 1")
+    if not mf_new.same_layout(mf_old):
+        raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
+    if mf_new.data.data_ptr() == mf_old.data.data_ptr():
+        raise ValueError("heat_step needs distinct old/new MultiFabs (double buffering)")
+    if verify and params.dt > params.stability_limit:
+        warnings.warn(f"dt={params.dt} exceeds stability bound {params.stability_limit}", stacklevel=2)
+    sched = _schedule_for(mf_old, schedule)
+    plan = schedule_sweep_plan(mf_old, sched, zmerge)
+    if plan.nblocks == 0:
+        return
+    dxi0, dxi1, dxi2, dtD = params.coefficients()
+    L = _native.load()
+    _native.check(L.tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr, 0, mf_old.ncomp,
+                                  dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
+
+
+def _check_poisson(phi: MultiFab, rhs: MultiFab):
+    if phi.nghost < 1:
+        raise ValueError("GSRB requires nghost >= 1 on phi")
+    if phi.ncomp != 1 or rhs.ncomp != 1:
+        raise ValueError("GSRB operates on single-component phi and rhs")
+    if phi.ba != rhs.ba or phi.local_units != rhs.local_units:
+        raise ValueError("phi and rhs must share the BoxArray and distribution")
+
+
+def gsrb_color(phi: MultiFab, rhs: MultiFab, geom: Geometry, color: int,
+               schedule: TileSchedule | None = None) -> None:
+    """In-place red (0) or black (1) update ``phi = (sum6(phi) + h2*rhs)/6``
+    on cells with ``(i+j+k)&1 == color``; h2 = dx*dx (cubic cells)."""
+    _check_poisson(phi, rhs)
+    if color not in (0, 1):
+        raise ValueError("color must be 0 (red) or 1 (black)")
+    h2 = geom.dx[0] * geom.dx[0]
+    plan = schedule_sweep_plan(phi, _schedule_for(phi, schedule))
+    if plan.nblocks == 0:
+        return
+    _native.check(_native.load().tm_gsrb_color(plan.handle, phi.layout.to_c(), phi.ptr, rhs.layout.to_c(),
+                                               rhs.ptr, color, h2, phi.stream()), "tm_gsrb_color")
+
+
+def gsrb_sweep(phi: MultiFab, rhs: MultiFab, geom: Geometry, schedule=None, plan=None) -> None:
+    """One sweep as BASELINE config 4 specifies: red, FillBoundary, black,
+    FillBoundary."""
+    from .multifab import fill_boundary
+
+    gsrb_color(phi, rhs, geom, 0, schedule)
+    fill_boundary(phi, geom, plan)
+    gsrb_color(phi, rhs, geom, 1, schedule)
+    fill_boundary(phi, geom, plan)
+
+
+def residual_maxnorm(phi: MultiFab, rhs: MultiFab, geom: Geometry, schedule=None, device_out=None):
+    """max over valid cells of ``|rhs + (sum6(phi) - 6 phi)/h2|``; ghosts of
+    phi must be filled.  Returns a Python float (or writes ``device_out``)."""
+    import torch
+
+    _check_poisson(phi, rhs)
+    h2 = geom.dx[0] * geom.dx[0]
+    plan = schedule_sweep_plan(phi, _schedule_for(phi, schedule))
+    out = device_out if device_out is not None else torch.zeros(1, dtype=torch.float64, device=phi.device)
+    if plan.nblocks:
+        _native.check(_native.load().tm_residual_maxnorm(plan.handle, phi.layout.to_c(), phi.ptr,
+                                                         rhs.layout.to_c(), rhs.ptr, h2, out.data_ptr(),
+                                                         phi.stream()), "tm_residual_maxnorm")
+    from .multifab import comm_info
+
+    if comm_info()[1] > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(out, op=dist.ReduceOp.MAX)
+    if device_out is not None:
+        return out
+    return float(out.item())
+
+
+def init_cosine(mf: MultiFab, geom: Geometry, modes=(1, 1, 1), offset: float = 0.0) -> None:
+    """Valid data = offset + product of per-dimension cosines at cell
+    centres: a discrete eigenfunction of the periodic 7-point operator
+    (reference kernels.py:345-362)."""
+    import numpy as np
+
+    dom = geom.domain
+    n = dom.extents
+
+    def fn(i, j, k):
+        return offset + (np.cos(2.0 * np.pi * modes[0] * (i - dom.lo[0] + 0.5) / n[0])
+                         * np.cos(2.0 * np.pi * modes[1] * (j - dom.lo[1] + 0.5) / n[1])
+                         * np.cos(2.0 * np.pi * modes[2] * (k - dom.lo[2] + 0.5) / n[2]))
+
+    for c in range(mf.ncomp):
+        mf.set_from_function(fn, c)
+
+
+def heat_amplification(params: HeatParams, geom: Geometry, modes=(1, 1, 1)) -> float:
+    """Exact per-step amplification of a cosine mode (kernels.py:365-377)."""
+    import math
+
+    n = geom.domain.extents
+    g = 1.0
+    for d in range(3):
+        theta = 2.0 * math.pi * modes[d] / n[d]
+        g += params.diffusivity * params.dt * (2.0 * math.cos(theta) - 2.0) / params.dx[d] ** 2
+    return g
