@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtilemesh_b200.so")
+LIB_PATH = os.environ.get("TILEMESH_LIB") or os.path.join(HERE, "libtilemesh_b200.so")
 
 TM_OK = 0
 TM_ERR_INVALID = 1

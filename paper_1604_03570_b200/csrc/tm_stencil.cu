@@ -39,6 +39,19 @@ struct SweepArgs {
     int32_t box_x, box_y, stage_elems;
 };
 
+// First column of the staged plane box.  TMA traps (illegal instruction) when
+// the innermost box coordinate is not 16-B aligned, so the box starts at the
+// even column at or below x0 - 1 and is wide enough for either parity.
+__device__ __forceinline__ int box_x_start(const tm_block &blk) { return (blk.x0 - 1) & ~1; }
+
+// Stage plane p (slot-local z = blk.z0 - 1 + p) of field w = slot*ncomp+comp.
+__device__ __forceinline__ void issue_plane(const CUtensorMap *map, double *dst, uint64_t *bar, const tm_block &blk,
+                                            int p, int w, uint32_t tx_bytes) {
+    using namespace tmk;
+    mbar_arrive_expect_tx(bar, tx_bytes);
+    tma_load_plane(dst, map, bar, box_x_start(blk), blk.y0 - 1, blk.z0 - 1 + p, w);
+}
+
 template <int OP, int NWARP, int SEGS>
 __global__ void __launch_bounds__(NWARP * 32) sweep_kernel(const __grid_constant__ CUtensorMap map, SweepArgs a) {
     using namespace tmk;
@@ -64,12 +77,12 @@ __global__ void __launch_bounds__(NWARP * 32) sweep_kernel(const __grid_constant
     if (tid == 0) {
         const int first = nplanes < kStages ? nplanes : kStages;
         for (int p = 0; p < first; ++p) {
-            mbar_arrive_expect_tx(&bars[p], tx_bytes);
-            tma_load_plane(stages + p * a.stage_elems, &map, &bars[p], blk.x0 - 1, blk.y0 - 1, blk.z0 - 1 + p, w);
+            issue_plane(&map, stages + p * a.stage_elems, &bars[p], blk, p, w, tx_bytes);
         }
     }
 
     // cells owned by this thread: segment s = warp + NWARP*q -> row s / nxs, x chunk s % nxs
+    const int xsh = blk.x0 - box_x_start(blk);  // 1 or 2: smem column of the tile's first cell
     const int nxs = (blk.nx + 31) >> 5;
     const int nseg = blk.ny * nxs;
     int sidx[SEGS], cx[SEGS], cy[SEGS];
@@ -82,7 +95,7 @@ __global__ void __launch_bounds__(NWARP * 32) sweep_kernel(const __grid_constant
         act[q] = (s < nseg) && (x < blk.nx);
         cx[q] = x;
         cy[q] = y;
-        sidx[q] = (y + 1) * bx + (x + 1);
+        sidx[q] = (y + 1) * bx + (x + xsh);
     }
 
     const Strides st = strides_of(a.L);
@@ -105,8 +118,7 @@ __global__ void __launch_bounds__(NWARP * 32) sweep_kernel(const __grid_constant
     for (int q = 0; q < SEGS; ++q) uc[q] = act[q] ? stages[(1 % kStages) * a.stage_elems + sidx[q]] : 0.0;
     __syncthreads();
     if (tid == 0 && kStages < nplanes) {
-        mbar_arrive_expect_tx(&bars[0], tx_bytes);
-        tma_load_plane(stages, &map, &bars[0], blk.x0 - 1, blk.y0 - 1, blk.z0 - 1 + kStages, w);
+        issue_plane(&map, stages, &bars[0], blk, kStages, w, tx_bytes);
     }
 
     double vmax = 0.0;
@@ -154,9 +166,7 @@ __global__ void __launch_bounds__(NWARP * 32) sweep_kernel(const __grid_constant
         __syncthreads();
         if (tid == 0 && pc + kStages < nplanes) {
             const int st_i = pc % kStages;
-            mbar_arrive_expect_tx(&bars[st_i], tx_bytes);
-            tma_load_plane(stages + st_i * a.stage_elems, &map, &bars[st_i], blk.x0 - 1, blk.y0 - 1,
-                           blk.z0 - 1 + pc + kStages, w);
+            issue_plane(&map, stages + st_i * a.stage_elems, &bars[st_i], blk, pc + kStages, w, tx_bytes);
         }
     }
 
@@ -214,7 +224,7 @@ int launch(const CUtensorMap &map, const SweepArgs &a, int cfg, int64_t nblocks,
 struct tm_sweep_plan {
     int64_t nblocks = 0;
     tm_block *d_blocks = nullptr;
-    int max_nx = 0, max_ny = 0, cfg = 0;
+    int max_nx = 0, max_ny = 0, max_seg = 0, cfg = 0;
     // small cache of encoded tensor maps keyed by (base pointer, layout)
     struct MapEntry {
         const double *base;
@@ -256,7 +266,10 @@ int prepare(tm_sweep_plan *p, const tm_layout *L, const double *base, const char
     if (rc) return rc;
     if (L->nghost < 1) return fail(TM_ERR_INVALID, std::string(who) + ": stencil requires nghost >= 1");
     if (!base) return fail(TM_ERR_INVALID, std::string(who) + ": null field");
-    const int bx = (p->max_nx + 2 + 1) & ~1;
+    // reductions accept any block; stencil sweeps need blocks that fit a CTA tile
+    if (p->max_nx + 4 > 256 || p->max_ny + 2 > 256 || p->max_seg > kMaxSegs)
+        return fail(TM_ERR_INVALID, std::string(who) + ": block exceeds the CTA tile limit (split it)");
+    const int bx = (p->max_nx + 3 + 1) & ~1;  // x0-2 .. x0+nx: covers both start parities
     const int by = p->max_ny + 2;
     rc = plane_map(p, *L, base, bx, by, map);
     if (rc) return rc;
@@ -289,12 +302,11 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
         my = std::max(my, k.ny);
         maxseg = std::max(maxseg, k.ny * ((k.nx + 31) / 32));
     }
-    if (mx + 2 > 256 || my + 2 > 256 || maxseg > kMaxSegs)
-        return fail(TM_ERR_INVALID, "tm_sweep_plan_create: block exceeds the CTA tile limit (split it)");
     tm_sweep_plan *p = new tm_sweep_plan();
     p->nblocks = nblocks;
     p->max_nx = mx;
     p->max_ny = my;
+    p->max_seg = maxseg;
     p->cfg = 3;
     for (int c = 0; c < 4; ++c)
         if (maxseg <= kCfgs[c].nwarp * kCfgs[c].segs) {
