@@ -28,13 +28,16 @@ __global__ void __launch_bounds__(32) serial_sum_kernel(const tm_block *__restri
     for (int k = 0; k < b.nz; ++k)
         for (int j = 0; j < b.ny; ++j) {
             const double *row = p0 + (int64_t)(b.z0 + k) * st.plane + (int64_t)(b.y0 + j) * st.row + b.x0;
-            for (int x = 0; x < b.nx; x += 32) {
-                const int n = min(32, b.nx - x);
+            int x = 0;
+            for (; x + 32 <= b.nx; x += 32) {  // full chunks: shuffles unrolled, only the adds chain
+                const double v = __ldg(row + x + lane);
+#pragma unroll
+                for (int l = 0; l < 32; ++l) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, l));
+            }
+            if (x < b.nx) {
+                const int n = b.nx - x;
                 const double v = lane < n ? __ldg(row + x + lane) : 0.0;
-                for (int l = 0; l < n; ++l) {
-                    const double t = __shfl_sync(0xffffffffu, v, l);
-                    total = __dadd_rn(total, t);
-                }
+                for (int l = 0; l < n; ++l) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, l));
             }
         }
     if (lane == 0) partial[blockIdx.x] = total;
