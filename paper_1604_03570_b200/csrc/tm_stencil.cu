@@ -16,7 +16,6 @@
 //   unew = uold + dtD*(((fxp-fxm)*dxi0 + (fyp-fym)*dxi1) + (fzp-fzm)*dxi2)
 // so results are bit-identical to the reference (no tolerance needed).
 #include <algorithm>
-#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -509,7 +508,7 @@ int tm_heat_sweep(tm_sweep_plan *plan, const tm_layout *layout, const double *uo
     a.c2 = dxi2;
     a.c3 = dtD;
     a.comp0 = comp0;
-    if (plan->vec > 0 && !getenv("TM_SCALAR_HEAT"))
+    if (plan->vec > 0)
         return launch_vec(*map, a, plan->vec, plan->nblocks, ncomp_sweep, smem, as_stream(stream));
     return launch<OP_HEAT>(*map, a, plan->cfg, plan->nblocks, ncomp_sweep, smem, as_stream(stream));
 }
