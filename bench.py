@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--zmerge", action="store_true", help="fuse z-stacked tiles into one CTA k-march")
+    ap.add_argument("--unfused", action="store_true",
+                    help="reference step structure (FillBoundary kernel + tiled sweep) instead of the fused step")
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -65,15 +67,16 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def profile_traffic(config_name: str):
-    """dram bytes per sweep launch from the committed ncu capture, if any."""
+def profile_traffic(config_name: str, fused: bool = False):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     try:
         with open(p) as fh:
             d = json.load(fh)
-        return d.get("heat_sweep", {}).get(config_name, {}).get("dram_bytes_per_launch")
+        key = "fused_step" if fused else "heat_sweep"
+        return d.get(key, {}).get(config_name, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
@@ -240,7 +243,8 @@ def run_ours(args, w):
     params = tm.HeatParams.stable(1.0, geom.dx)
     plan = tm.build_fill_plan(mf, geom)
     sched = tm.build_schedule(mf, w.tile_size)
-    runner = HeatRunner(mf, geom, params, sched, plan, use_graph=not args.no_graph, zmerge=args.zmerge)
+    runner = HeatRunner(mf, geom, params, sched, plan, use_graph=not args.no_graph, zmerge=args.zmerge,
+                        fused=False if args.unfused else None)
     local_cells = sum(ba[u].ncells for u in mf.local_units) * w.ncomp
     total_cells = w.cells * w.ncomp
 
@@ -265,24 +269,39 @@ def run_ours(args, w):
     ms_max = float(t.item())
     value = total_cells * args.steps / (ms_max * 1e-3)
 
-    # --- dominant kernel: per-launch sweep / fill times (eager, events) --
-    cur = runner.current
-    other = runner.b if cur is runner.a else runner.a
-    nrep = 50
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(3 * nrep)]
-    barrier()
-    for r in range(nrep):
-        evs[3 * r].record(stream)
-        tm.fill_boundary(cur, geom, plan)
-        evs[3 * r + 1].record(stream)
-        tm.heat_step(other, cur, geom, params, sched, zmerge=args.zmerge)
-        evs[3 * r + 2].record(stream)
-        cur, other = other, cur
-    barrier()
-    fill_ms = sum(evs[3 * r].elapsed_time(evs[3 * r + 1]) for r in range(nrep)) / nrep
-    sweep_ms = sum(evs[3 * r + 1].elapsed_time(evs[3 * r + 2]) for r in range(nrep)) / nrep
+    # --- per-launch kernel times (eager, CUDA events on the launching stream) --
+    # The GPU queue stays ahead of the Python issue loop (each launch is tens of
+    # microseconds of device time), so event deltas are device time.
+    def timed(fn, nrep=40):
+        cur = runner.current
+        other = runner.b if cur is runner.a else runner.a
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(nrep + 1)]
+        for _ in range(3):
+            fn(cur, other)
+            cur, other = other, cur
+        barrier()
+        evs[0].record(stream)
+        for r in range(nrep):
+            fn(cur, other)
+            cur, other = other, cur
+            evs[r + 1].record(stream)
+        barrier()
+        return sum(evs[r].elapsed_time(evs[r + 1]) for r in range(nrep)) / nrep
+
+    if runner.fused:
+        def fused_step(o, n):
+            runner.fh.step(n, o, params)
+        runner.fh.prime(runner.current, plan)
+        kern_ms = timed(fused_step)
+        kern_name = "march_kernel<PACKED,SCATTER> (tm_heat_march: sweep + fused face-halo exchange)"
+    fill_ms = timed(lambda o, n: tm.fill_boundary(o, geom, plan))
+    sweep_ms = timed(lambda o, n: tm.heat_step(n, o, geom, params, sched, zmerge=args.zmerge))
+    if not runner.fused:
+        kern_ms = sweep_ms
+        kern_name = "heat_vec_kernel / sweep_kernel<heat> (tm_heat_sweep)"
+    runner.reset()  # state was advanced outside the runner's bookkeeping
     peak, peak_src = peaks()
-    achieved = BYTES_PER_CELL * local_cells / (sweep_ms * 1e-3) / 1e9
+    achieved = BYTES_PER_CELL * local_cells / (kern_ms * 1e-3) / 1e9
     ghost_cells = sum(t.dst_box.ncells for t in plan.tags if mf.dm[t.dst_unit] == mf.rank) * w.ncomp
     fill_gbs = 16 * ghost_cells / (fill_ms * 1e-3) / 1e9
 
@@ -299,7 +318,7 @@ def run_ours(args, w):
     for _ in range(e2e_runs):
         g = glob_pinned.to(dev, non_blocking=True)
         runner.a.from_global(g)
-        runner.steps_done = 0
+        runner.reset()
         out = runner.advance(job_steps)
         csum = out.reduce_sum_device()
         host_out.copy_(out.to_global())
@@ -321,8 +340,8 @@ def run_ours(args, w):
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, sample, _, _, _ = cpu_reference_rate(w, args.cpu_seconds)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
-        traffic = profile_traffic(w.name)
-        launches_per_step = 2 + (2 if world > 1 else 0)
+        traffic = profile_traffic(w.name, runner.fused)
+        launches_per_step = runner.launches_per_step + (2 if world > 1 else 0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
@@ -334,15 +353,20 @@ def run_ours(args, w):
                 "l2": f"inputs larger than L2: {2 * total_cells * 8 / 1e6:.0f} MB streamed per step vs 126 MB L2",
                 "parallelism": f"dm{world} (contiguous box slabs)", "cuda_graph": runner.use_graph,
                 "zmerge": args.zmerge,
+                "step_impl": ("fused: one persistent column-march launch per step; the epilogue writes face halos "
+                              "of the next step (FillBoundary fused), edges/corners refreshed by one FillBoundary "
+                              "per advance()" if runner.fused else
+                              "FillBoundary kernel + tiled heat sweep (2 launches per step)"),
             },
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": "sweep_kernel<heat> (tm_heat_sweep)",
-                "bytes_per_launch": BYTES_PER_CELL * local_cells, "avg_launch_ms": sweep_ms,
+                "traffic": traffic, "kernel": kern_name,
+                "bytes_per_launch": BYTES_PER_CELL * local_cells, "avg_launch_ms": kern_ms,
                 "peak_source": peak_src,
             },
-            "fill": {"avg_launch_ms": fill_ms, "ghost_gbs": fill_gbs, "ghost_cells": ghost_cells,
-                     "share_of_step": fill_ms / (fill_ms + sweep_ms)},
+            "unfused_components": {"fill_boundary_ms": fill_ms, "fill_ghost_gbs": fill_gbs,
+                                   "ghost_cells": ghost_cells, "tiled_sweep_ms": sweep_ms,
+                                   "note": "reference step structure, for comparison"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / job_steps,
                     "d2h_bytes_per_step": d2h / job_steps,
                     "job": f"upload phi0 (pinned) + {job_steps} steps + download phi + checksum",

@@ -126,6 +126,26 @@ int tm_residual_maxnorm(tm_sweep_plan *plan, const tm_layout *phi_layout, const 
                         const tm_layout *rhs_layout, const double *rhs, double h2, double *d_out,
                         void *stream);
 
+/* ---- persistent column-march heat sweep (Kernel A2) -------------------------
+ * Replaces the same reference call as tm_heat_sweep (compiled.py:84-99 via
+ * kernels.py:174-215) with a different CTA decomposition: `columns` are box
+ * tiles spanning the full z extent (tm_block with nz = box nz); `nctas`
+ * persistent CTAs each march an equal share of all column planes.
+ * Columns must start on an even x and have even width <= 128, height <= 64. */
+typedef struct tm_march_plan tm_march_plan;
+int tm_march_plan_create(const tm_block *columns, int64_t ncolumns, int32_t nctas, tm_march_plan **out);
+int tm_march_plan_destroy(tm_march_plan *plan);
+/* xh_old == NULL: x halos from the ghost columns of uold (FillBoundary must
+ * have run).  xh_old != NULL: x halos from the packed buffer
+ * xh[(slot*ncomp+c)][z][side][y] (valid y,z extents; side 0 = i = lo-1,
+ * side 1 = i = hi+1).  xh_new != NULL additionally scatters every box's
+ * boundary values into its face neighbours' halos in unew / xh_new
+ * (d_nbr: 6 neighbour slots per slot, order -x,+x,-y,+y,-z,+z, -1 = none):
+ * the fused FillBoundary of the next step.  Face halos only (7-point). */
+int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                  int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
+                  const double *xh_old, double *xh_new, const int32_t *d_nbr, void *stream);
+
 /* ---- reductions (one block per unit, blocks in grid order) --------------- */
 /* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =
  * serial sum of the partials in block order: bit-identical to the

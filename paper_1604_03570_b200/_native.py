@@ -45,6 +45,7 @@ EXPORTS = [
     "tm_copy_plan_create", "tm_copy_plan_destroy", "tm_copy_plan_elements", "tm_copy_run",
     "tm_sweep_plan_create", "tm_sweep_plan_destroy", "tm_heat_sweep", "tm_gsrb_color",
     "tm_residual_maxnorm", "tm_reduce_sum", "tm_reduce_minmax",
+    "tm_march_plan_create", "tm_march_plan_destroy", "tm_heat_march",
 ]
 
 _lib = None
@@ -81,6 +82,9 @@ def load():
     L.tm_residual_maxnorm.argtypes = [vp, P(tm_layout), vp, P(tm_layout), vp, f64, vp, vp]
     L.tm_reduce_sum.argtypes = [vp, P(tm_layout), vp, i32, vp, vp, vp]
     L.tm_reduce_minmax.argtypes = [vp, P(tm_layout), vp, i32, vp, vp]
+    L.tm_march_plan_create.argtypes = [vp, i64, i32, P(vp)]
+    L.tm_march_plan_destroy.argtypes = [vp]
+    L.tm_heat_march.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("tm_last_error", "tm_abi_version", "tm_copy_plan_elements"):
             getattr(L, name).restype = ctypes.c_int
@@ -147,4 +151,25 @@ class SweepPlan:
         h = getattr(self, "handle", None)
         if h is not None and _lib is not None:
             _lib.tm_sweep_plan_destroy(h)
+            self.handle = None
+
+
+class MarchPlan:
+    """Library-owned column/segment tables of the persistent sweep (``tm_march_plan``)."""
+
+    def __init__(self, columns: np.ndarray, nctas: int):
+        L = load()
+        columns = np.ascontiguousarray(columns, dtype=BLOCK_DTYPE)
+        h = ctypes.c_void_p()
+        check(L.tm_march_plan_create(columns.ctypes.data if len(columns) else None, len(columns), nctas,
+                                     ctypes.byref(h)), "tm_march_plan_create")
+        self.handle = h
+        self.ncolumns = len(columns)
+        self.nctas = nctas
+        self.columns = columns
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and _lib is not None:
+            _lib.tm_march_plan_destroy(h)
             self.handle = None

@@ -1,0 +1,495 @@
+// Kernel A2: persistent column-march heat sweep.
+//
+// Why: on B200 the halo rows/planes that neighbouring tile-CTAs share are not
+// served from L2 (profiles/l2_experiments_r01.md) -- a 64x8x8 tile re-reads
+// 1.65x its bytes from DRAM.  Here each CTA owns whole tile *columns* (the
+// full z extent of a box's x-y tile) and marches through them, so every plane
+// of the column is read once and the z halo costs 2 planes per column, not 2
+// per tile.  The grid is persistent (a few CTAs per SM); CTA i takes a
+// contiguous, equal share of all column planes, split into segments, and the
+// TMA ring keeps streaming across segment boundaries.
+//
+// Two halo sources for x:
+//   STD    -- the x ghost cells in the rows (same layout as Kernel A);
+//   PACKED -- a packed x-halo buffer xh[slot*ncomp+c][z][side][y] (dense), so
+//             rows are loaded exactly [x0, x0+nx) and the two ghost columns
+//             cost 16 B per row instead of two 64-B DRAM blocks.
+// With SCATTER the epilogue also writes each box's boundary values into its
+// face neighbours' halos of the NEW field (y/z ghost rows/planes of unew and
+// the packed x halo xh_new), so the next step needs no FillBoundary for
+// intra-GPU neighbours.  The 7-point stencil needs face
+// halos only; edge/corner ghosts are not touched on this path.
+//
+// Arithmetic is identical to Kernel A (reference flux form, FMA-free).
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "tm_common.cuh"
+
+namespace {
+
+constexpr int kStages = 4;
+
+struct Segment {
+    int32_t col;     // column index
+    int32_t k0, k1;  // local planes [k0, k1) of the column
+    int32_t reserved;
+};
+
+struct MarchArgs {
+    const tm_block *cols;
+    const Segment *segs;
+    const int32_t *seg_begin;  // per CTA: segments [seg_begin[i], seg_begin[i+1])
+    double *out;
+    tm_layout L;
+    double c0, c1, c2, c3;
+    int32_t box_x, box_y, stage_elems;  // plane box (doubles) and stage stride
+    int32_t xh_off;                     // offset of the x-halo slice inside a stage (PACKED)
+    int32_t nyv, nzv;                   // packed x-halo extents (valid y, z of a slot)
+    double *xh_new;                     // SCATTER: packed x halo of the new field
+    const int32_t *nbr;                 // SCATTER: 6 neighbour slots per slot (-x,+x,-y,+y,-z,+z)
+};
+
+// Plane sequence of a CTA: for each of its segments, planes k0-1 .. k1 (k1-k0+2 planes).
+struct PlaneCursor {
+    int seg, q;  // segment index (absolute) and plane index within the segment
+};
+
+template <bool PACKED>
+__device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap *xmap, const MarchArgs &a,
+                                      double *stage, uint64_t *bar, const tm_block &c, int comp, int z,
+                                      uint32_t tx_bytes) {
+    using namespace tmk;
+    const int w = c.slot * a.L.ncomp + comp;
+    mbar_arrive_expect_tx(bar, tx_bytes);
+    if (PACKED) {
+        tma_load_plane(stage, map, bar, c.x0, c.y0 - 1, z, w);
+        // x halo: y range of the column, both sides, valid plane z - nghost
+        const int g = a.L.nghost;
+        tma_load_plane(stage + a.xh_off, xmap, bar, c.y0 - g, 0, z - g, w);
+    } else {
+        tma_load_plane(stage, map, bar, (c.x0 - 1) & ~1, c.y0 - 1, z, w);
+    }
+}
+
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER>
+__global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant__ CUtensorMap map,
+                                                           const __grid_constant__ CUtensorMap xmap, MarchArgs a) {
+    using namespace tmk;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *stages = reinterpret_cast<double *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kStages * a.stage_elems * sizeof(double));
+
+    const int comp = blockIdx.y;
+    const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
+    if (s_begin >= s_end) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bx = a.box_x;
+    const uint32_t tx_bytes =
+        (uint32_t)((a.box_x * a.box_y + (PACKED ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
+
+    // ---- producer state (thread 0): next plane to issue ----
+    PlaneCursor pc{s_begin, 0};
+    int issued = 0;  // global plane index of the next issue
+    auto issue_next = [&](int stage_idx) {
+        const Segment sg = a.segs[pc.seg];
+        const tm_block c = a.cols[sg.col];
+        issue<PACKED>(&map, &xmap, a, stages + stage_idx * a.stage_elems, &bars[stage_idx], c, comp,
+                      c.z0 + sg.k0 - 1 + pc.q, tx_bytes);
+        ++issued;
+        if (++pc.q == sg.k1 - sg.k0 + 2) {
+            ++pc.seg;
+            pc.q = 0;
+        }
+    };
+    int total = 0;  // planes in this CTA's sequence
+    for (int s = s_begin; s < s_end; ++s) total += a.segs[s].k1 - a.segs[s].k0 + 2;
+
+    if (tid == 0) {
+        prefetch_tensormap(&map);
+        if (PACKED) prefetch_tensormap(&xmap);
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < kStages && s < total; ++s) issue_next(s);
+
+    // release plane g (all consumers done with it) and refill its stage with g + kStages
+    auto release = [&](int g) {
+        __syncthreads();
+        if (tid == 0 && g + kStages < total) issue_next(g % kStages);
+    };
+    auto wait_plane = [&](int g) { mbar_wait(&bars[g % kStages], (g / kStages) & 1); };
+
+    const double c0 = a.c0, c1 = a.c1, c2 = a.c2, c3 = a.c3;
+    const Strides st = strides_of(a.L);
+    const int g_ng = a.L.nghost;
+    const int xsh = PACKED ? 0 : 2;  // smem column of a column's first cell (x0 is even)
+    int g = 0;                       // global plane index of the current segment's first plane
+
+    for (int s = s_begin; s < s_end; ++s) {
+        const Segment sg = a.segs[s];
+        const tm_block c = a.cols[sg.col];
+        const bool lane_on = lane * CPL < c.nx;
+        int ci[RPW];
+        bool on[RPW];
+        double *optr[RPW];
+        // SCATTER targets hoisted out of the k loop (null = this row/lane has no face there)
+        double *yptr[RPW];
+        double *xlp[RPW], *xrp[RPW];
+        const int64_t obase = (int64_t)c.slot * st.slot + (int64_t)comp * st.comp +
+                              (int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + lane * CPL;
+        const int nyb = a.nyv, nzb = a.nzv;
+        const int32_t *nb = a.nbr + 6 * c.slot;
+        const int zl0 = c.z0 - g_ng + sg.k0;  // valid z index of the segment's first plane
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = warp * RPW + i;
+            on[i] = lane_on && r < c.ny;
+            ci[i] = (min(r, c.ny - 1) + 1) * bx + min(lane * CPL, c.nx - CPL) + xsh;
+            optr[i] = a.out + obase + (int64_t)r * st.row;
+            yptr[i] = nullptr;
+            xlp[i] = xrp[i] = nullptr;
+            if (SCATTER && on[i]) {
+                const int yl = c.y0 - g_ng + r;
+                if (yl == 0 && nb[2] >= 0) yptr[i] = optr[i] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
+                if (yl == nyb - 1 && nb[3] >= 0)
+                    yptr[i] = optr[i] + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
+                const int xl0 = c.x0 - a.L.xoff + lane * CPL;
+                if (xl0 == 0 && nb[0] >= 0)  // our x=0 column -> the -x neighbour's right halo
+                    xlp[i] = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb + yl;
+                if (xl0 + CPL == c.nx && nb[1] >= 0)
+                    xrp[i] = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb + yl;
+            }
+        }
+        // priming: planes k0-1 and k0 -> carried z flux and centre values
+        double uc[RPW][CPL], fzm[RPW][CPL];
+        wait_plane(g);
+        wait_plane(g + 1);
+        {
+            const double *s0 = stages + (g % kStages) * a.stage_elems;
+            const double *s1 = stages + ((g + 1) % kStages) * a.stage_elems;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const double lo = s0[ci[i] + j], hi = s1[ci[i] + j];
+                    uc[i][j] = hi;
+                    fzm[i][j] = rn_mul(rn_sub(hi, lo), c2);
+                }
+            }
+        }
+        release(g);
+        const int nk = sg.k1 - sg.k0;
+        for (int kk = 0; kk < nk; ++kk) {
+            const int gc = g + 1 + kk, gn = g + 2 + kk;
+            const double *sc = stages + (gc % kStages) * a.stage_elems;
+            const double *sn = stages + (gn % kStages) * a.stage_elems;
+            const double *xh = sc + a.xh_off;  // PACKED: [side][y] of the centre plane
+            const int64_t po = (int64_t)kk * st.plane;
+            const int64_t xo = (int64_t)kk * 2 * nyb;
+            // z faces: uniform per plane
+            const int zl = zl0 + kk;
+            int64_t zoff = 0;
+            bool zs = false;
+            if (SCATTER) {
+                if (zl == 0 && nb[4] >= 0) {
+                    zs = true;
+                    zoff = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
+                } else if (zl == nzb - 1 && nb[5] >= 0) {
+                    zs = true;
+                    zoff = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
+                }
+            }
+            wait_plane(gn);
+            // compute every row branch-free (rows past the column are clamped to a valid smem
+            // row and simply not stored) so the compiler can interleave all RPW*CPL chains
+            double out[RPW][CPL];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const int r = min(warp * RPW + i, c.ny - 1);
+                const double *cp = sc + ci[i];
+                double ym[CPL], yp[CPL], un[CPL];
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    if constexpr (CPL >= 2) {
+                        const double2 m2 = *reinterpret_cast<const double2 *>(cp - bx + j);
+                        const double2 p2 = *reinterpret_cast<const double2 *>(cp + bx + j);
+                        const double2 n2 = *reinterpret_cast<const double2 *>(sn + ci[i] + j);
+                        ym[j] = m2.x, ym[j + 1] = m2.y;
+                        yp[j] = p2.x, yp[j + 1] = p2.y;
+                        un[j] = n2.x, un[j + 1] = n2.y;
+                    } else {
+                        ym[j] = cp[j - bx];
+                        yp[j] = cp[j + bx];
+                        un[j] = sn[ci[i] + j];
+                    }
+                }
+                double xl, xr;
+                if (PACKED) {
+                    xl = (lane == 0) ? xh[r] : cp[-1];
+                    xr = (lane * CPL + CPL == c.nx) ? xh[(a.box_y - 2) + r] : cp[CPL];
+                } else {
+                    xl = cp[-1];
+                    xr = cp[CPL];
+                }
+                double fx[CPL + 1];
+                fx[0] = rn_mul(rn_sub(uc[i][0], xl), c0);
+#pragma unroll
+                for (int j = 1; j < CPL; ++j) fx[j] = rn_mul(rn_sub(uc[i][j], uc[i][j - 1]), c0);
+                fx[CPL] = rn_mul(rn_sub(xr, uc[i][CPL - 1]), c0);
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const double u0 = uc[i][j];
+                    const double fym = rn_mul(rn_sub(u0, ym[j]), c1), fyp = rn_mul(rn_sub(yp[j], u0), c1);
+                    const double fzp = rn_mul(rn_sub(un[j], u0), c2);
+                    double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fyp, fym), c1));
+                    sum = rn_add(sum, rn_mul(rn_sub(fzp, fzm[i][j]), c2));
+                    out[i][j] = rn_add(u0, rn_mul(c3, sum));
+                    fzm[i][j] = fzp;
+                    uc[i][j] = un[j];
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (!on[i]) continue;
+                double *o = optr[i] + po;
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    if constexpr (CPL >= 2)
+                        *reinterpret_cast<double2 *>(o + j) = make_double2(out[i][j], out[i][j + 1]);
+                    else
+                        o[j] = out[i][j];
+                }
+                if (SCATTER) {
+                    if (yptr[i]) {
+#pragma unroll
+                        for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                            if constexpr (CPL >= 2)
+                                *reinterpret_cast<double2 *>(yptr[i] + po + j) = make_double2(out[i][j], out[i][j + 1]);
+                            else
+                                yptr[i][po + j] = out[i][j];
+                        }
+                    }
+                    if (zs) {
+#pragma unroll
+                        for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                            if constexpr (CPL >= 2)
+                                *reinterpret_cast<double2 *>(o + zoff + j) = make_double2(out[i][j], out[i][j + 1]);
+                            else
+                                o[zoff + j] = out[i][j];
+                        }
+                    }
+                    if (xlp[i]) xlp[i][xo] = out[i][0];
+                    if (xrp[i]) xrp[i][xo] = out[i][CPL - 1];
+                }
+            }
+            release(gc);
+        }
+        release(g + nk + 1);
+        g += nk + 2;
+    }
+}
+
+}  // namespace
+
+struct tm_march_plan {
+    int64_t ncols = 0, nsegs = 0;
+    int32_t nctas = 0;
+    tm_block *d_cols = nullptr;
+    Segment *d_segs = nullptr;
+    int32_t *d_seg_begin = nullptr;
+    int max_nx = 0, max_ny = 0;
+    bool even = true;
+};
+
+namespace {
+
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER>
+int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int nctas, int ncomp,
+                     size_t smem, cudaStream_t s) {
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(march)");
+        configured = true;
+    }
+    kern<<<dim3(nctas, ncomp), NWARP * 32, smem, s>>>(map, xmap, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return tmk::cuda_fail(e, "march launch");
+    return TM_OK;
+}
+
+template <bool PACKED, bool SCATTER>
+int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int cpl, int rows, int nctas,
+                 int ncomp, size_t smem, cudaStream_t s) {
+    // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 8x4, 64 -> 16x4
+    if (cpl == 2) {
+        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    }
+    if (cpl == 4) {
+        if (rows <= 8) return launch_march_one<4, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<4, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    }
+    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    return launch_march_one<1, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+}
+
+int encode_xh_map(CUtensorMap *map, const tm_layout &L, const double *xh, int box_y) {
+    // packed x halo: dims (nyv, 2, nzv, nslots*ncomp), box (box_y, 2, 1, 1)
+    tm_layout X{};
+    X.nslots = L.nslots;
+    X.ncomp = L.ncomp;
+    X.nghost = 0;
+    X.pitch = L.ny - 2 * L.nghost;  // nyv doubles per "row"
+    X.ny = 2;
+    X.nz = L.nz - 2 * L.nghost;
+    X.xoff = 0;
+    return tmk::encode_plane_map(map, X, xh, box_y, 2);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_march_plan_create(const tm_block *cols, int64_t ncols, int32_t nctas, tm_march_plan **out) {
+    using namespace tmk;
+    if (!out) return fail(TM_ERR_INVALID, "tm_march_plan_create: null out");
+    *out = nullptr;
+    if (ncols < 0 || (ncols > 0 && !cols) || nctas < 1)
+        return fail(TM_ERR_INVALID, "tm_march_plan_create: bad arguments");
+    int64_t total = 0;
+    int mx = 1, my = 1;
+    bool even = true;
+    for (int64_t c = 0; c < ncols; ++c) {
+        const tm_block &k = cols[c];
+        if (k.nx < 1 || k.ny < 1 || k.nz < 1 || k.x0 < 2 || k.y0 < 1 || k.z0 < 1)
+            return fail(TM_ERR_INVALID, "tm_march_plan_create: malformed column " + std::to_string(c));
+        total += k.nz;
+        mx = std::max(mx, k.nx);
+        my = std::max(my, k.ny);
+        even = even && (k.x0 % 2 == 0) && (k.nx % 2 == 0);
+    }
+    if (mx > 128 || my > 64) return fail(TM_ERR_INVALID, "tm_march_plan_create: column exceeds 128 x 64");
+    // equal contiguous shares of the column planes (reference partition rule, iterator.py:93-103)
+    std::vector<Segment> segs;
+    std::vector<int32_t> begin(nctas + 1, 0);
+    int64_t col = 0, k = 0;
+    for (int32_t i = 0; i < nctas; ++i) {
+        begin[i] = (int32_t)segs.size();
+        const int64_t q = total / nctas, r = total % nctas;
+        int64_t left = q + (i < r ? 1 : 0);
+        while (left > 0 && col < ncols) {
+            const int64_t take = std::min<int64_t>(left, cols[col].nz - k);
+            segs.push_back(Segment{(int32_t)col, (int32_t)k, (int32_t)(k + take), 0});
+            k += take;
+            left -= take;
+            if (k == cols[col].nz) {
+                ++col;
+                k = 0;
+            }
+        }
+    }
+    begin[nctas] = (int32_t)segs.size();
+    tm_march_plan *p = new tm_march_plan();
+    p->ncols = ncols;
+    p->nsegs = (int64_t)segs.size();
+    p->nctas = nctas;
+    p->max_nx = mx;
+    p->max_ny = my;
+    p->even = even;
+    cudaError_t e = cudaMalloc(&p->d_cols, sizeof(tm_block) * std::max<int64_t>(ncols, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_segs, sizeof(Segment) * std::max<size_t>(segs.size(), 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->d_seg_begin, sizeof(int32_t) * (nctas + 1));
+    if (e == cudaSuccess && ncols) e = cudaMemcpy(p->d_cols, cols, sizeof(tm_block) * ncols, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !segs.empty())
+        e = cudaMemcpy(p->d_segs, segs.data(), sizeof(Segment) * segs.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(p->d_seg_begin, begin.data(), sizeof(int32_t) * (nctas + 1), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(p->d_cols);
+        cudaFree(p->d_segs);
+        cudaFree(p->d_seg_begin);
+        delete p;
+        return cuda_fail(e, "tm_march_plan_create");
+    }
+    *out = p;
+    return TM_OK;
+}
+
+int tm_march_plan_destroy(tm_march_plan *p) {
+    if (!p) return TM_OK;
+    cudaFree(p->d_cols);
+    cudaFree(p->d_segs);
+    cudaFree(p->d_seg_begin);
+    delete p;
+    return TM_OK;
+}
+
+int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
+                  double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old, double *xh_new,
+                  const int32_t *d_nbr, void *stream) {
+    using namespace tmk;
+    if (!p) return fail(TM_ERR_INVALID, "tm_heat_march: null plan");
+    int rc = check_layout(layout, "tm_heat_march");
+    if (rc) return rc;
+    const tm_layout &L = *layout;
+    if (L.nghost < 1 || !uold || !unew || uold == unew)
+        return fail(TM_ERR_INVALID, "tm_heat_march: needs nghost >= 1 and distinct old/new fields");
+    if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march: bad ncomp");
+    const bool packed = xh_old != nullptr;
+    const bool scatter = xh_new != nullptr;
+    if (scatter && (!packed || !d_nbr)) return fail(TM_ERR_INVALID, "tm_heat_march: scatter needs xh_old and nbr");
+    if (p->ncols == 0) return TM_OK;
+    if (!p->even) return fail(TM_ERR_INVALID, "tm_heat_march: columns must start on even x and have even width");
+    MarchArgs a{};
+    a.cols = p->d_cols;
+    a.segs = p->d_segs;
+    a.seg_begin = p->d_seg_begin;
+    a.out = unew;
+    a.L = L;
+    a.c0 = dxi0;
+    a.c1 = dxi1;
+    a.c2 = dxi2;
+    a.c3 = dtD;
+    a.box_x = packed ? p->max_nx : p->max_nx + 4;
+    a.box_y = p->max_ny + 2;
+    a.nyv = L.ny - 2 * L.nghost;
+    a.nzv = L.nz - 2 * L.nghost;
+    a.xh_off = ((a.box_x * a.box_y + 15) / 16) * 16;
+    const int stage = packed ? a.xh_off + ((2 * p->max_ny + 15) / 16) * 16 : a.xh_off;
+    a.stage_elems = stage;
+    a.xh_new = xh_new;
+    a.nbr = d_nbr;
+    const size_t smem = (size_t)kStages * stage * sizeof(double) + kStages * sizeof(uint64_t);
+    if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_heat_march: column plane too large for shared memory");
+    CUtensorMap map, xmap;
+    rc = encode_plane_map(&map, L, uold, a.box_x, a.box_y);
+    if (rc) return rc;
+    if (packed) {
+        if (p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_heat_march: packed x halo needs even column height");
+        rc = encode_xh_map(&xmap, L, xh_old, p->max_ny);
+        if (rc) return rc;
+    } else {
+        xmap = map;
+    }
+    const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
+    if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
+    cudaStream_t s = as_stream(stream);
+    if (!packed) return launch_march<false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (!scatter) return launch_march<true, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    return launch_march<true, true>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+}
+
+}  // extern "C"

@@ -1,0 +1,249 @@
+"""Persistent column-march sweep (Kernel A2) and the fused halo path.
+
+Host side of ``csrc/tm_march.cu``:
+
+* ``march_columns`` cuts every local box into full-width x columns of at
+  most ``max_rows`` rows spanning the whole box in z (the CTA work unit of
+  the march kernel; results do not depend on the cut -- same arithmetic per
+  cell as the reference, bit for bit);
+* ``heat_march`` runs one sweep with x halos read from the ghost columns
+  (after a regular FillBoundary);
+* ``FusedHalo`` keeps packed x-halo buffers and a face-neighbour table for a
+  pair of MultiFabs so that a step is ONE launch: the sweep reads face halos
+  written by the previous step's epilogue and scatters its own boundary
+  values into the neighbours' halos of the new field (the fused FillBoundary
+  of SURVEY.md §7.9).  Edge/corner ghosts are not needed by the 7-point
+  stencil and are only refreshed by ``finalize`` (a regular FillBoundary).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .box import Box
+from .boxarray import BoxIndex, Geometry
+from .multifab import MultiFab, cell_offsets
+
+SMEM_BUDGET = 220 * 1024
+STAGES = 4
+
+
+def sm_count(device) -> int:
+    import torch
+
+    return torch.cuda.get_device_properties(device).multi_processor_count
+
+
+def _even_chunks(n: int, cap: int) -> list:
+    """Split n into ceil(n/cap) near-equal EVEN chunks (n even)."""
+    parts = -(-n // cap)
+    pairs = n // 2
+    q, r = divmod(pairs, parts)
+    out = []
+    pos = 0
+    for p in range(parts):
+        sz = 2 * (q + (p < r))
+        out.append((pos, sz))
+        pos += sz
+    return out
+
+
+DEFAULT_ROWS = 16  # measured best on C2 (tools/march_perf.py, profiles/march_r01.txt)
+
+
+def max_rows_for(nx: int, packed: bool) -> int:
+    width = nx if packed else nx + 4
+    per_stage = SMEM_BUDGET // STAGES // 8 - (2 * 64 if packed else 0)
+    rows = per_stage // width - 2
+    rows = min(DEFAULT_ROWS, rows)
+    return max(2, rows - rows % 2)
+
+
+def march_eligible(mf: MultiFab) -> bool:
+    L = mf.layout
+    if mf.nghost < 1 or not mf.local_units:
+        return False
+    for u in mf.local_units:
+        e = mf.units[u].valid.extents
+        if e[0] % 2 or e[0] > 128:
+            return False
+    return L.xoff % 2 == 0
+
+
+def march_columns(mf: MultiFab, max_rows: int | None = None, packed: bool = False) -> np.ndarray:
+    L = mf.layout
+    rows = []
+    for u in mf.local_units:
+        v = mf.units[u].valid
+        nx, ny, nz = v.extents
+        cap = max_rows or max_rows_for(nx, packed)
+        if ny % 2 == 0:
+            chunks = _even_chunks(ny, cap)
+        else:
+            if packed:
+                raise ValueError("packed x halos need boxes of even y extent")
+            n = -(-ny // cap)
+            base, rem = divmod(ny, n)
+            chunks, pos = [], 0
+            for p in range(n):
+                sz = base + (p < rem)
+                chunks.append((pos, sz))
+                pos += sz
+        s = mf.slot_of[u]
+        for (y0, sz) in chunks:
+            rows.append((s, L.xoff, L.nghost + y0, L.nghost, nx, sz, nz, (v.lo[0] + v.lo[1] + y0 + v.lo[2]) & 1))
+    out = np.zeros(len(rows), dtype=_native.BLOCK_DTYPE)
+    arr = np.array(rows, dtype=np.int64).reshape(-1, 8)
+    for n, name in enumerate(_native.BLOCK_DTYPE.names):
+        out[name] = arr[:, n]
+    return out
+
+
+def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool) -> int:
+    nx = int(columns["nx"].max())
+    ny = int(columns["ny"].max())
+    width = nx if packed else nx + 4
+    stage = -(-(width * (ny + 2)) // 16) * 16 + (-(-2 * ny // 16) * 16 if packed else 0)
+    smem = STAGES * stage * 8 + 64
+    threads = {8: 128, 16: 256, 32: 256, 64: 512}[min(k for k in (8, 16, 32, 64) if ny <= k)]
+    return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 128)))
+
+
+def march_plan(mf: MultiFab, packed: bool = False, max_rows: int | None = None,
+               nctas: int | None = None) -> "_native.MarchPlan":
+    key = ("march", packed, max_rows, nctas, mf.layout, tuple(mf.local_units))
+    plan = mf._plans.get(key)
+    if plan is None:
+        cols = march_columns(mf, max_rows, packed)
+        n = nctas or sm_count(mf.device) * ctas_per_sm(mf, cols, packed)
+        plan = _native.MarchPlan(cols, n)
+        mf._plans[key] = plan
+    return plan
+
+
+def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None = None,
+               nctas: int | None = None) -> None:
+    """One sweep (all components) with x halos from the ghost columns of
+    ``mf_old``; FillBoundary must have run.  Bit-identical to heat_step."""
+    if mf_old.nghost < 1:
+        raise ValueError("heat kernel requires nghost >= 1")
+    if not mf_new.same_layout(mf_old):
+        raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
+    if not march_eligible(mf_old):
+        raise ValueError("column march needs boxes of even x extent <= 128")
+    plan = march_plan(mf_old, False, max_rows, nctas)
+    c = params.coefficients()
+    _native.check(_native.load().tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
+                                               mf_old.ncomp, c[0], c[1], c[2], c[3], None, None, None,
+                                               mf_old.stream()), "tm_heat_march")
+
+
+# --------------------------------------------------------------------------
+# fused halo path
+# --------------------------------------------------------------------------
+def face_neighbors(mf: MultiFab, geom: Geometry):
+    """Per local slot, the slots of the 6 face neighbours (-x,+x,-y,+y,-z,+z),
+    or None when the layout is not fusable: every face must be covered by
+    exactly one LOCAL box of identical extents (uniform chopped domains,
+    periodic or interior faces)."""
+    valids = [u.valid for u in mf.units]
+    index = BoxIndex(valids)
+    dom = geom.domain
+    n = dom.extents
+    table = np.full((len(mf.local_units), 6), -1, dtype=np.int32)
+    for s, u in enumerate(mf.local_units):
+        v = valids[u]
+        e = v.extents
+        for d in range(3):
+            for side in (0, 1):
+                shift = [0, 0, 0]
+                shift[d] = -e[d] if side == 0 else e[d]
+                lo = [v.lo[k] + shift[k] for k in range(3)]
+                img = list(lo)
+                if not (dom.lo[d] <= lo[d] and lo[d] + e[d] - 1 <= dom.hi[d]):
+                    if not geom.periodic[d]:
+                        return None
+                    img[d] = dom.lo[d] + (lo[d] - dom.lo[d]) % n[d]
+                target = Box(img, [img[k] + e[k] - 1 for k in range(3)])
+                hits = index.query(target)
+                if len(hits) != 1 or valids[hits[0]] != target:
+                    return None
+                nb = hits[0]
+                if nb not in mf.slot_of:
+                    return None
+                table[s, 2 * d + side] = mf.slot_of[nb]
+    return table
+
+
+def fusable(mf: MultiFab, geom: Geometry) -> bool:
+    if not march_eligible(mf):
+        return False
+    ext = {mf.units[u].valid.extents for u in mf.local_units}
+    if len(ext) != 1:
+        return False
+    (nx, ny, nz), = ext
+    L = mf.layout
+    if ny % 2 or (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
+        return False
+    return face_neighbors(mf, geom) is not None
+
+
+class FusedHalo:
+    """Packed x halos + neighbour table shared by an old/new MultiFab pair."""
+
+    def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, max_rows: int | None = None,
+                 nctas: int | None = None):
+        import torch
+
+        if not (fusable(a, geom) and a.same_layout(b)):
+            raise ValueError("layout is not eligible for the fused halo path")
+        self.geom = geom
+        L = a.layout
+        self.nyv = L.ny - 2 * L.nghost
+        self.nzv = L.nz - 2 * L.nghost
+        nc = a.ncomp
+        shape = (L.nslots * nc, self.nzv, 2, self.nyv)
+        self.xh = {id(a): torch.zeros(shape, dtype=torch.float64, device=a.device),
+                   id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
+        table = face_neighbors(a, geom)
+        self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=a.device)
+        self.plan = march_plan(a, True, max_rows, nctas)
+        self._init_plan = self._xh_init_plan(a, table)
+
+    def _xh_init_plan(self, mf: MultiFab, table) -> "_native.CopyPlan":
+        L = mf.layout
+        tags = np.zeros(2 * len(mf.local_units), dtype=_native.COPY_TAG_DTYPE)
+        slot_unit = {s: u for u, s in mf.slot_of.items()}
+        k = 0
+        for s, u in enumerate(mf.local_units):
+            v = mf.units[u].valid
+            nx, ny, nz = v.extents
+            for side in (0, 1):
+                nb = slot_unit[int(table[s, side])]
+                nv = mf.units[nb].valid
+                col = nv.hi[0] if side == 0 else nv.lo[0]  # left halo <- left neighbour's last column
+                src = cell_offsets(mf, np.array([nb]), np.array([[col, nv.lo[1], nv.lo[2]]]))[0]
+                dst = ((s * mf.ncomp) * self.nzv * 2 + side) * self.nyv
+                tags[k] = (dst, src, 1, ny, nz, 0)
+                k += 1
+        self.xh_side = (1, 2 * self.nyv, 2 * self.nyv * self.nzv)
+        return _native.CopyPlan(tags, mf.ncomp)
+
+    def prime(self, mf: MultiFab, plan=None) -> None:
+        """Fill every halo of ``mf`` from its valid data (regular FillBoundary
+        + packed x halos)."""
+        from .multifab import fill_boundary
+
+        fill_boundary(mf, self.geom, plan)
+        xh = self.xh[id(mf)]
+        self._init_plan.run(xh.data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
+
+    def step(self, new: MultiFab, old: MultiFab, params) -> None:
+        """One fused step: sweep old -> new reading old's face halos and
+        writing new's face halos (no separate FillBoundary)."""
+        c = params.coefficients()
+        _native.check(_native.load().tm_heat_march(
+            self.plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
+            self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), old.stream()),
+            "tm_heat_march(fused)")

@@ -1,16 +1,25 @@
-"""Step loops: ``steps x (FillBoundary; sweep)`` as one CUDA graph.
+"""Step loops: ``steps x (FillBoundary; sweep)`` captured as CUDA graphs.
 
 The reference's driver loop (bench.py:198-206) calls ``fill_boundary`` and
 ``heat_step`` from Python every step.  On the GPU a step of config C2 is
-~50 us of device time, comparable to the Python + ctypes cost of issuing
-it, so ``HeatRunner`` captures the double-buffered pair of steps
-(old -> new, new -> old) once into a CUDA graph and replays it.  Every
-launch inside the graph is one of the library kernels, with arguments (and
-TMA descriptors) frozen at capture time; the buffers never move, so replay
-is exact.
+tens of microseconds of device time, comparable to the Python + ctypes cost
+of issuing it, so ``HeatRunner`` captures a double-buffered pair of steps
+(old -> new, new -> old) once into a CUDA graph and replays it.  Every launch
+inside the graph is a library kernel with arguments (and TMA descriptors)
+frozen at capture time; the buffers never move, so replay is exact.
 
-Multi-rank runs (NCCL halo exchange) step eagerly: the exchange is issued
-through torch.distributed between the pack and unpack kernels.
+Two step implementations, bit-identical in the valid cells:
+
+* ``fused=False`` -- the reference's structure: FillBoundary (Kernel B)
+  then the tiled sweep (Kernel A), two launches per step;
+* ``fused=True``  -- one launch per step: the persistent column-march sweep
+  reads face halos that the previous step's epilogue wrote and scatters its
+  own boundary values into the neighbours' halos (``march.FusedHalo``).
+  Edge/corner ghosts (unused by the 7-point stencil) are refreshed by one
+  regular FillBoundary at the end of ``advance``, so the MultiFab handed
+  back has every ghost filled.
+
+Multi-rank runs (NCCL halo exchange) step eagerly with ``fused=False``.
 """
 
 from __future__ import annotations
@@ -26,7 +35,10 @@ class HeatRunner:
     """Owns the old/new pair and advances it ``n`` steps at a time."""
 
     def __init__(self, mf: MultiFab, geom: Geometry, params: HeatParams, schedule=None,
-                 plan: FillPlan | None = None, use_graph: bool | None = None, zmerge: bool = False):
+                 plan: FillPlan | None = None, use_graph: bool | None = None, zmerge: bool = False,
+                 fused: bool | None = None, march_rows: int | None = None):
+        from . import march
+
         self.geom = geom
         self.params = params
         self.a = mf
@@ -38,16 +50,34 @@ class HeatRunner:
         self.zmerge = zmerge
         world = comm_info()[1]
         self.use_graph = (world == 1) if use_graph is None else (use_graph and world == 1)
+        can_fuse = world == 1 and march.fusable(mf, geom)
+        if fused and not can_fuse:
+            raise ValueError("fused halo path needs one rank and a uniform fully-covered box layout")
+        self.fused = can_fuse if fused is None else fused
+        self.fh = march.FusedHalo(self.a, self.b, geom, march_rows) if self.fused else None
         self._graph = None
+        self._primed = False
         self.steps_done = 0
 
     @property
     def current(self) -> MultiFab:
         return self.a if self.steps_done % 2 == 0 else self.b
 
+    @property
+    def launches_per_step(self) -> int:
+        return 1 if self.fused else 2
+
+    def reset(self) -> None:
+        """Call after modifying ``a`` from outside: restart at step 0."""
+        self.steps_done = 0
+        self._primed = False
+
     def _step(self, old: MultiFab, new: MultiFab) -> None:
-        fill_boundary(old, self.geom, self.plan)
-        heat_step(new, old, self.geom, self.params, self.schedule, zmerge=self.zmerge)
+        if self.fused:
+            self.fh.step(new, old, self.params)
+        else:
+            fill_boundary(old, self.geom, self.plan)
+            heat_step(new, old, self.geom, self.params, self.schedule, zmerge=self.zmerge)
 
     def _capture(self):
         import torch
@@ -65,32 +95,33 @@ class HeatRunner:
                 self._step(self.b, self.a)
         torch.cuda.current_stream().wait_stream(s)
         self._graph = g
-        self.launches_per_pair = 4
 
-    def advance(self, n: int) -> MultiFab:
-        """Advance ``n`` steps; returns the MultiFab holding the state."""
+    def advance(self, n: int, finalize: bool = True) -> MultiFab:
+        """Advance ``n`` steps; returns the MultiFab holding the state (all
+        ghosts filled when ``finalize``)."""
+        if self.fused and not self._primed:
+            self.fh.prime(self.current, self.plan)
+            self._primed = True
         k = 0
-        if self.use_graph and n >= 2:
-            if self._graph is None:
-                # capture runs two real steps; account for them
-                if self.steps_done % 2:
-                    self._step(self.b, self.a)
-                    self.steps_done += 1
-                    k += 1
-                self._capture()
-                self.steps_done += 2
-                k += 2
-            if self.steps_done % 2 and k < n:
+        if self.use_graph:
+            if self.steps_done % 2 and n - k >= 3:  # realign to the captured a -> b -> a pair
                 self._step(self.b, self.a)
                 self.steps_done += 1
                 k += 1
-            while n - k >= 2:
-                self._graph.replay()
-                self.steps_done += 2
-                k += 2
+            if self.steps_done % 2 == 0 and n - k >= 2:
+                if self._graph is None:
+                    self._capture()  # runs two real steps
+                    self.steps_done += 2
+                    k += 2
+                while n - k >= 2:
+                    self._graph.replay()
+                    self.steps_done += 2
+                    k += 2
         while k < n:
             old, new = (self.a, self.b) if self.steps_done % 2 == 0 else (self.b, self.a)
             self._step(old, new)
             self.steps_done += 1
             k += 1
+        if self.fused and finalize:
+            fill_boundary(self.current, self.geom, self.plan)
         return self.current

@@ -75,12 +75,14 @@ def main():
             j = json.load(open(jpath))
         except (OSError, ValueError):
             j = {}
-        sweeps = [d for d in summary if "sweep" in d["kernel"] or "heat" in d["kernel"]]
+        jkey = sys.argv[sys.argv.index("--jkey") + 1] if "--jkey" in sys.argv else "heat_sweep"
+        match = sys.argv[sys.argv.index("--match") + 1] if "--match" in sys.argv else "sweep"
+        sweeps = [d for d in summary if match in d["kernel"]]
         if sweeps:
             d = sweeps[0]
             rb = float(d["dram__bytes_read.sum"][0]) * SCALE.get(d["dram__bytes_read.sum"][1], 1)
             wb = float(d["dram__bytes_write.sum"][0]) * SCALE.get(d["dram__bytes_write.sum"][1], 1)
-            j.setdefault("heat_sweep", {})[key] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb,
+            j.setdefault(jkey, {})[key] = {"dram_bytes_per_launch": rb + wb, "dram_read": rb,
                                                    "dram_write": wb, "source": dst, "kernel": d["kernel"]}
             json.dump(j, open(jpath, "w"), indent=1)
 
