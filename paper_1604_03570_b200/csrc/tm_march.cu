@@ -73,13 +73,20 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
     }
 }
 
+// Warp-specialised pipeline: warps 0..NWARP-1 compute, warp NWARP is the TMA
+// producer.  full[s] completes when stage s holds its plane (TMA transaction
+// bytes); empty[s] completes when all NWARP consumer warps released it.  No
+// CTA-wide barrier in the steady state: fast warps run ahead up to the ring
+// depth while the producer refills each stage as soon as it is free.
 template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER>
-__global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant__ CUtensorMap map,
-                                                           const __grid_constant__ CUtensorMap xmap, MarchArgs a) {
+__global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
+                                                                 const __grid_constant__ CUtensorMap xmap,
+                                                                 MarchArgs a) {
     using namespace tmk;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kStages * a.stage_elems * sizeof(double));
+    uint64_t *empty = bars + kStages;
 
     const int comp = blockIdx.y;
     const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
@@ -89,38 +96,40 @@ __global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant
     const uint32_t tx_bytes =
         (uint32_t)((a.box_x * a.box_y + (PACKED ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
 
-    // ---- producer state (thread 0): next plane to issue ----
-    PlaneCursor pc{s_begin, 0};
-    int issued = 0;  // global plane index of the next issue
-    auto issue_next = [&](int stage_idx) {
-        const Segment sg = a.segs[pc.seg];
-        const tm_block c = a.cols[sg.col];
-        issue<PACKED>(&map, &xmap, a, stages + stage_idx * a.stage_elems, &bars[stage_idx], c, comp,
-                      c.z0 + sg.k0 - 1 + pc.q, tx_bytes);
-        ++issued;
-        if (++pc.q == sg.k1 - sg.k0 + 2) {
-            ++pc.seg;
-            pc.q = 0;
-        }
-    };
-    int total = 0;  // planes in this CTA's sequence
-    for (int s = s_begin; s < s_end; ++s) total += a.segs[s].k1 - a.segs[s].k0 + 2;
-
     if (tid == 0) {
         prefetch_tensormap(&map);
         if (PACKED) prefetch_tensormap(&xmap);
 #pragma unroll
-        for (int s = 0; s < kStages; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&empty[s], NWARP);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    if (tid == 0)
-        for (int s = 0; s < kStages && s < total; ++s) issue_next(s);
 
-    // release plane g (all consumers done with it) and refill its stage with g + kStages
+    if (warp == NWARP) {  // ---------------- producer warp ----------------
+        if (lane == 0) {
+            int p = 0;
+            for (int s = s_begin; s < s_end; ++s) {
+                const Segment sg = a.segs[s];
+                const tm_block c = a.cols[sg.col];
+                const int n = sg.k1 - sg.k0 + 2;
+                for (int q = 0; q < n; ++q, ++p) {
+                    const int st_i = p % kStages;
+                    if (p >= kStages) mbar_wait(&empty[st_i], ((p / kStages) - 1) & 1);
+                    issue<PACKED>(&map, &xmap, a, stages + st_i * a.stage_elems, &bars[st_i], c, comp,
+                                  c.z0 + sg.k0 - 1 + q, tx_bytes);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
     auto release = [&](int g) {
-        __syncthreads();
-        if (tid == 0 && g + kStages < total) issue_next(g % kStages);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[g % kStages]);
     };
     auto wait_plane = [&](int g) { mbar_wait(&bars[g % kStages], (g / kStages) & 1); };
 
@@ -138,8 +147,13 @@ __global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant
         bool on[RPW];
         double *optr[RPW];
         // SCATTER targets hoisted out of the k loop (null = this row/lane has no face there)
-        double *yptr[RPW];
-        double *xlp[RPW], *xrp[RPW];
+        // y faces: at most one row per column has yl == 0 (-y face) or yl == nyb-1 (+y face);
+        // its neighbour ghost row is o + ydelta.  x faces: the lane holding x = 0 / x = nx-1
+        // writes into the neighbour's packed halo at xh_base + yl (+ xstep per plane).
+        int yface[RPW];  // 0 none, 1 -y, 2 +y
+        int ylv[RPW];
+        int64_t ydl = 0, ydh = 0;
+        double *xhl = nullptr, *xhr = nullptr;
         const int64_t obase = (int64_t)c.slot * st.slot + (int64_t)comp * st.comp +
                               (int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + lane * CPL;
         const int nyb = a.nyv, nzb = a.nzv;
@@ -151,112 +165,117 @@ __global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant
             on[i] = lane_on && r < c.ny;
             ci[i] = (min(r, c.ny - 1) + 1) * bx + min(lane * CPL, c.nx - CPL) + xsh;
             optr[i] = a.out + obase + (int64_t)r * st.row;
-            yptr[i] = nullptr;
-            xlp[i] = xrp[i] = nullptr;
+            yface[i] = 0;
+            ylv[i] = c.y0 - g_ng + r;
             if (SCATTER && on[i]) {
-                const int yl = c.y0 - g_ng + r;
-                if (yl == 0 && nb[2] >= 0) yptr[i] = optr[i] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
-                if (yl == nyb - 1 && nb[3] >= 0)
-                    yptr[i] = optr[i] + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
-                const int xl0 = c.x0 - a.L.xoff + lane * CPL;
-                if (xl0 == 0 && nb[0] >= 0)  // our x=0 column -> the -x neighbour's right halo
-                    xlp[i] = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb + yl;
-                if (xl0 + CPL == c.nx && nb[1] >= 0)
-                    xrp[i] = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb + yl;
+                if (ylv[i] == 0 && nb[2] >= 0) yface[i] = 1;
+                if (ylv[i] == nyb - 1 && nb[3] >= 0) yface[i] = 2;
             }
         }
+        if (SCATTER) {
+            ydl = (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
+            ydh = (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
+            const int xl0 = c.x0 - a.L.xoff + lane * CPL;
+            if (lane_on && xl0 == 0 && nb[0] >= 0)  // our x=0 column -> the -x neighbour's right halo
+                xhl = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb;
+            if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0)
+                xhr = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb;
+        }
+        // ---- per-segment invariants: shared-memory byte offsets of this lane's operands ----
+        const uint32_t sbase = smem_u32(stages);
+        const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
+        const uint32_t ystep = (uint32_t)bx * 8u;
+        uint32_t roff[RPW], xlo[RPW], xro[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = min(warp * RPW + i, c.ny - 1);
+            roff[i] = (uint32_t)ci[i] * 8u;
+            const bool left_edge = PACKED && lane == 0;
+            const bool right_edge = PACKED && (min(lane * CPL, c.nx - CPL) + CPL == c.nx);
+            xlo[i] = left_edge ? (uint32_t)(a.xh_off + r) * 8u : roff[i] - 8u;
+            xro[i] = right_edge ? (uint32_t)(a.xh_off + (a.box_y - 2) + r) * 8u : roff[i] + (uint32_t)CPL * 8u;
+        }
+        const int64_t pstep = st.plane;  // doubles per plane (output pointers)
+        const int64_t xstep = 2 * (int64_t)nyb;
+
         // priming: planes k0-1 and k0 -> carried z flux and centre values
-        double uc[RPW][CPL], fzm[RPW][CPL];
+        double ua[RPW][CPL], ub[RPW][CPL], fzm[RPW][CPL];
         wait_plane(g);
         wait_plane(g + 1);
         {
-            const double *s0 = stages + (g % kStages) * a.stage_elems;
-            const double *s1 = stages + ((g + 1) % kStages) * a.stage_elems;
+            const uint32_t s0 = sbase + (uint32_t)(g % kStages) * sbytes;
+            const uint32_t s1 = sbase + (uint32_t)((g + 1) % kStages) * sbytes;
 #pragma unroll
-            for (int i = 0; i < RPW; ++i) {
+            for (int i = 0; i < RPW; ++i)
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
-                    const double lo = s0[ci[i] + j], hi = s1[ci[i] + j];
-                    uc[i][j] = hi;
+                    const double lo = lds_f64(s0 + roff[i] + 8u * j), hi = lds_f64(s1 + roff[i] + 8u * j);
+                    ua[i][j] = hi;
                     fzm[i][j] = rn_mul(rn_sub(hi, lo), c2);
                 }
-            }
         }
         release(g);
         const int nk = sg.k1 - sg.k0;
-        for (int kk = 0; kk < nk; ++kk) {
-            const int gc = g + 1 + kk, gn = g + 2 + kk;
-            const double *sc = stages + (gc % kStages) * a.stage_elems;
-            const double *sn = stages + (gn % kStages) * a.stage_elems;
-            const double *xh = sc + a.xh_off;  // PACKED: [side][y] of the centre plane
-            const int64_t po = (int64_t)kk * st.plane;
-            const int64_t xo = (int64_t)kk * 2 * nyb;
-            // z faces: uniform per plane
-            const int zl = zl0 + kk;
-            int64_t zoff = 0;
-            bool zs = false;
-            if (SCATTER) {
-                if (zl == 0 && nb[4] >= 0) {
-                    zs = true;
-                    zoff = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
-                } else if (zl == nzb - 1 && nb[5] >= 0) {
-                    zs = true;
-                    zoff = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
-                }
+        // z faces: plane index (within the segment) whose values go to a z neighbour's ghost plane
+        int kz_lo = -1, kz_hi = -1;
+        int64_t zoff_lo = 0, zoff_hi = 0;
+        if (SCATTER) {
+            if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
+                kz_lo = -zl0;
+                zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
             }
+            if (nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
+                kz_hi = nzb - 1 - zl0;
+                zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
+            }
+        }
+        // one plane: centre values in cur, next-plane values land in nxt
+        auto plane = [&](int kk, double (&cur)[RPW][CPL], double (&nxt)[RPW][CPL]) {
+            const int gc = g + 1 + kk, gn = g + 2 + kk;
+            const uint32_t sc = sbase + (uint32_t)(gc % kStages) * sbytes;
+            const uint32_t sn = sbase + (uint32_t)(gn % kStages) * sbytes;
             wait_plane(gn);
-            // compute every row branch-free (rows past the column are clamped to a valid smem
-            // row and simply not stored) so the compiler can interleave all RPW*CPL chains
             double out[RPW][CPL];
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
-                const int r = min(warp * RPW + i, c.ny - 1);
-                const double *cp = sc + ci[i];
-                double ym[CPL], yp[CPL], un[CPL];
+                double ym[CPL], yp[CPL];
+                const uint32_t cp = sc + roff[i];
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2) {
-                        const double2 m2 = *reinterpret_cast<const double2 *>(cp - bx + j);
-                        const double2 p2 = *reinterpret_cast<const double2 *>(cp + bx + j);
-                        const double2 n2 = *reinterpret_cast<const double2 *>(sn + ci[i] + j);
-                        ym[j] = m2.x, ym[j + 1] = m2.y;
-                        yp[j] = p2.x, yp[j + 1] = p2.y;
-                        un[j] = n2.x, un[j + 1] = n2.y;
+                        lds_f64x2(cp - ystep + 8u * j, ym[j], ym[j + 1]);
+                        lds_f64x2(cp + ystep + 8u * j, yp[j], yp[j + 1]);
+                        lds_f64x2(sn + roff[i] + 8u * j, nxt[i][j], nxt[i][j + 1]);
                     } else {
-                        ym[j] = cp[j - bx];
-                        yp[j] = cp[j + bx];
-                        un[j] = sn[ci[i] + j];
+                        ym[j] = lds_f64(cp - ystep + 8u * j);
+                        yp[j] = lds_f64(cp + ystep + 8u * j);
+                        nxt[i][j] = lds_f64(sn + roff[i] + 8u * j);
                     }
                 }
-                double xl, xr;
-                if (PACKED) {
-                    xl = (lane == 0) ? xh[r] : cp[-1];
-                    xr = (lane * CPL + CPL == c.nx) ? xh[(a.box_y - 2) + r] : cp[CPL];
-                } else {
-                    xl = cp[-1];
-                    xr = cp[CPL];
-                }
+                const double xl = lds_f64(sc + xlo[i]);
+                const double xr = lds_f64(sc + xro[i]);
                 double fx[CPL + 1];
-                fx[0] = rn_mul(rn_sub(uc[i][0], xl), c0);
+                fx[0] = rn_mul(rn_sub(cur[i][0], xl), c0);
 #pragma unroll
-                for (int j = 1; j < CPL; ++j) fx[j] = rn_mul(rn_sub(uc[i][j], uc[i][j - 1]), c0);
-                fx[CPL] = rn_mul(rn_sub(xr, uc[i][CPL - 1]), c0);
+                for (int j = 1; j < CPL; ++j) fx[j] = rn_mul(rn_sub(cur[i][j], cur[i][j - 1]), c0);
+                fx[CPL] = rn_mul(rn_sub(xr, cur[i][CPL - 1]), c0);
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
-                    const double u0 = uc[i][j];
+                    const double u0 = cur[i][j];
                     const double fym = rn_mul(rn_sub(u0, ym[j]), c1), fyp = rn_mul(rn_sub(yp[j], u0), c1);
-                    const double fzp = rn_mul(rn_sub(un[j], u0), c2);
+                    const double fzp = rn_mul(rn_sub(nxt[i][j], u0), c2);
                     double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fyp, fym), c1));
                     sum = rn_add(sum, rn_mul(rn_sub(fzp, fzm[i][j]), c2));
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
                     fzm[i][j] = fzp;
-                    uc[i][j] = un[j];
                 }
             }
+            // all shared reads of the centre plane are done: hand its stage back early
+            release(gc);
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 if (!on[i]) continue;
-                double *o = optr[i] + po;
+                double *o = optr[i];
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2)
@@ -265,30 +284,34 @@ __global__ void __launch_bounds__(NWARP * 32) march_kernel(const __grid_constant
                         o[j] = out[i][j];
                 }
                 if (SCATTER) {
-                    if (yptr[i]) {
+                    double *zo = nullptr;
+                    if (kk == kz_lo) zo = o + zoff_lo;
+                    if (kk == kz_hi) zo = o + zoff_hi;
+                    double *yo = yface[i] == 0 ? nullptr : o + (yface[i] == 1 ? ydl : ydh);
+#pragma unroll
+                    for (int t = 0; t < 2; ++t) {
+                        double *d = t == 0 ? yo : zo;
+                        if (!d) continue;
 #pragma unroll
                         for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                             if constexpr (CPL >= 2)
-                                *reinterpret_cast<double2 *>(yptr[i] + po + j) = make_double2(out[i][j], out[i][j + 1]);
+                                *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
                             else
-                                yptr[i][po + j] = out[i][j];
+                                d[j] = out[i][j];
                         }
                     }
-                    if (zs) {
-#pragma unroll
-                        for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
-                            if constexpr (CPL >= 2)
-                                *reinterpret_cast<double2 *>(o + zoff + j) = make_double2(out[i][j], out[i][j + 1]);
-                            else
-                                o[zoff + j] = out[i][j];
-                        }
-                    }
-                    if (xlp[i]) xlp[i][xo] = out[i][0];
-                    if (xrp[i]) xrp[i][xo] = out[i][CPL - 1];
+                    if (xhl) xhl[(int64_t)kk * xstep + ylv[i]] = out[i][0];
+                    if (xhr) xhr[(int64_t)kk * xstep + ylv[i]] = out[i][CPL - 1];
                 }
+                optr[i] += pstep;
             }
-            release(gc);
+        };
+        int kk = 0;
+        for (; kk + 1 < nk; kk += 2) {  // ping-pong: no register rotation
+            plane(kk, ua, ub);
+            plane(kk + 1, ub, ua);
         }
+        if (kk < nk) plane(kk, ua, ub);
         release(g + nk + 1);
         g += nk + 2;
     }
@@ -318,7 +341,7 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const Marc
         if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(march)");
         configured = true;
     }
-    kern<<<dim3(nctas, ncomp), NWARP * 32, smem, s>>>(map, xmap, a);
+    kern<<<dim3(nctas, ncomp), (NWARP + 1) * 32, smem, s>>>(map, xmap, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march launch");
     return TM_OK;
@@ -472,7 +495,7 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     a.stage_elems = stage;
     a.xh_new = xh_new;
     a.nbr = d_nbr;
-    const size_t smem = (size_t)kStages * stage * sizeof(double) + kStages * sizeof(uint64_t);
+    const size_t smem = (size_t)kStages * stage * sizeof(double) + 2 * kStages * sizeof(uint64_t);
     if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_heat_march: column plane too large for shared memory");
     CUtensorMap map, xmap;
     rc = encode_plane_map(&map, L, uold, a.box_x, a.box_y);

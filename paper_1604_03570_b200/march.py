@@ -105,9 +105,9 @@ def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool) -> int:
     ny = int(columns["ny"].max())
     width = nx if packed else nx + 4
     stage = -(-(width * (ny + 2)) // 16) * 16 + (-(-2 * ny // 16) * 16 if packed else 0)
-    smem = STAGES * stage * 8 + 64
-    threads = {8: 128, 16: 256, 32: 256, 64: 512}[min(k for k in (8, 16, 32, 64) if ny <= k)]
-    return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 128)))
+    smem = STAGES * stage * 8 + 128
+    threads = 32 + {8: 128, 16: 256, 32: 256, 64: 512}[min(k for k in (8, 16, 32, 64) if ny <= k)]
+    return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 100)))
 
 
 def march_plan(mf: MultiFab, packed: bool = False, max_rows: int | None = None,

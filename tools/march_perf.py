@@ -49,3 +49,30 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def packed_noscatter(cfg="C2", rows=16, nctas=296):
+    """PACKED x halos, no scatter (isolates the epilogue's cost)."""
+    from paper_1604_03570_b200 import _native
+
+    w = tm.CONFIGS[cfg]
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    a = tm.MultiFab(ba, w.ncomp, w.nghost)
+    a.from_global(tm.make_init(w))
+    b = a.clone_empty()
+    p = tm.HeatParams.stable(1.0, geom.dx)
+    fh = march.FusedHalo(a, b, geom, rows, nctas)
+    fh.prime(a)
+    c = p.coefficients()
+
+    def go():
+        _native.check(_native.load().tm_heat_march(fh.plan.handle, a.layout.to_c(), a.ptr, b.ptr, a.ncomp, c[0], c[1],
+                                                   c[2], c[3], fh.xh[id(a)].data_ptr(), None, None, a.stream()), "m")
+    ms = graph_time(go, 20)
+    print(f"{cfg} packed-noscatter rows={rows} nctas={nctas}: {ms * 1e3:.1f} us")
+
+
+if "--noscatter" in sys.argv:
+    for r, n in ((16, 296), (16, 592), (8, 444)):
+        packed_noscatter("C2", r, n)
