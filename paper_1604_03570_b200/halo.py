@@ -50,6 +50,21 @@ def tag_elements(tag, ncomp: int) -> int:
     return e[0] * e[1] * e[2] * ncomp
 
 
+def message_layout(tags, groups, ncomp: int):
+    """Packed buffer layout of the messages in ``groups`` ({peer: [tag ids]}):
+    ``(rows, spans, total)`` with rows = [(tag id, element offset)] in buffer
+    order and spans = [(peer, offset, count)].  Inside a tag the elements are
+    x fastest, then y, z, component (the ``tm_side`` packed format)."""
+    rows, spans, off = [], [], 0
+    for peer, ids in groups.items():
+        start = off
+        for n in ids:
+            rows.append((n, off))
+            off += tag_elements(tags[n], ncomp)
+        spans.append((peer, start, off - start))
+    return rows, spans, off
+
+
 class HaloExchange:
     """Pack / grouped send-recv / unpack for one (MultiFab layout, plan)."""
 
@@ -64,17 +79,8 @@ class HaloExchange:
         nc = mf.ncomp
 
         def build(groups, remote_side_is_dst):
-            rows = []
-            spans = []
-            off = 0
-            for peer, ids in groups.items():
-                start = off
-                for n in ids:
-                    t = tags[n]
-                    e = t[1].extents
-                    rows.append((t, off, e))
-                    off += e[0] * e[1] * e[2] * nc
-                spans.append((peer, start, off - start))
+            layout, spans, off = message_layout(tags, groups, nc)
+            rows = [(tags[n], o, tags[n][1].extents) for n, o in layout]
             arr = np.zeros(len(rows), dtype=_native.COPY_TAG_DTYPE)
             if rows:
                 units = np.array([r[0][2] if remote_side_is_dst else r[0][0] for r in rows], dtype=np.int64)
