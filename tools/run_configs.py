@@ -1,0 +1,121 @@
+"""Run BASELINE configs C1-C5 at full size on one GPU: rates + size-independent
+parity properties.
+
+    python tools/run_configs.py [C1 C2 C3 C4 C5] [--oracle]
+
+Per heat config: fused and unfused step paths (independent kernels) must agree
+bit for bit; each component's sum is conserved (flux form) to 1e-11
+relative; C1/C2 checksums equal the reference's (golden / SURVEY value).
+C4 (GSRB): residual decreases; with --oracle the final phi and residual are
+compared bit for bit with the whole-domain numpy restatement.
+Prints one JSON line per config.
+"""
+
+import json
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1604_03570_b200 as tm  # noqa: E402
+from paper_1604_03570_b200.runner import HeatRunner  # noqa: E402
+
+REF_SUMS = {"C2": 16870634.63599003}  # SURVEY.md §8a a10 (reference run)
+
+
+def ev_time(fn):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) * 1e-3
+
+
+def heat_config(name):
+    w = tm.CONFIGS[name]
+    t0 = time.time()
+    glob = tm.make_init(w)
+    t_init = time.time() - t0
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    t0 = time.time()
+    mf = tm.MultiFab(ba, w.ncomp, w.nghost)
+    plan = tm.build_fill_plan(mf, geom)
+    t_plan = time.time() - t0
+    g = torch.from_numpy(glob).cuda()
+    del glob
+    sums0 = [float(torch.sum(g[c]).item()) for c in range(w.ncomp)]
+    p = tm.HeatParams.stable(1.0, geom.dx)
+    sched = tm.build_schedule(mf, w.tile_size)
+    res = {"config": name, "cells": w.cells * w.ncomp, "steps": w.steps, "init_s": t_init, "plan_s": t_plan}
+    finals = {}
+    for fused in (True, False):
+        mf.from_global(g)
+        r = HeatRunner(mf, geom, p, sched, plan, fused=fused)
+        r.advance(2)  # warm + capture
+        mf.from_global(g)
+        r.reset()
+        secs = ev_time(lambda: r.advance(w.steps))
+        out = r.current
+        key = "fused" if fused else "unfused"
+        res[key + "_rate"] = w.cells * w.ncomp * w.steps / secs
+        res[key + "_ms_per_step"] = secs / w.steps * 1e3
+        finals[key] = out.to_global()
+        res[key + "_sums"] = [out.reduce_sum(c) for c in range(w.ncomp)]
+        del r
+        torch.cuda.empty_cache()
+    res["fused_equals_unfused"] = bool(torch.equal(finals["fused"], finals["unfused"]))
+    res["conservation_max_rel"] = max(abs(s - s0) / abs(s0) for s, s0 in zip(res["fused_sums"], sums0))
+    if name in REF_SUMS:
+        res["checksum_equals_reference"] = res["fused_sums"][0] == REF_SUMS[name]
+    if name == "C1":
+        z = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "heat.npz"))
+        res["checksum_equals_reference"] = res["fused_sums"][0] == float(z["C1/sums"][-1][0])
+    return res
+
+
+def gsrb_config(oracle: bool):
+    w = tm.CONFIGS["C4"]
+    rhs_g = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    phi = tm.MultiFab(ba, 1, 1)
+    rhs = tm.MultiFab(ba, 1, 0)
+    rhs.from_global(rhs_g)
+    plan = tm.build_fill_plan(phi, geom)
+    sched = tm.build_schedule(phi, w.tile_size)
+    tm.gsrb_sweep(phi, rhs, geom, sched, plan)  # warm
+    phi.fill(0.0)
+    r0 = tm.residual_maxnorm(phi, rhs, geom, sched)
+    secs = ev_time(lambda: [tm.gsrb_sweep(phi, rhs, geom, sched, plan) for _ in range(w.steps)])
+    r1 = tm.residual_maxnorm(phi, rhs, geom, sched)
+    res = {"config": "C4", "cells": w.cells, "sweeps": w.steps, "rate": w.cells * w.steps / secs,
+           "ms_per_sweep": secs / w.steps * 1e3, "residual0": r0, "residual": r1, "residual_decreased": r1 < r0}
+    if oracle:
+        from oracle import oracle as orc
+
+        ref_phi, ref_res = orc.gsrb_periodic(np.zeros((w.n,) * 3), rhs_g[0], w.steps, w.dx * w.dx)
+        res["phi_equals_oracle"] = bool(np.array_equal(phi.to_global().cpu().numpy()[0], ref_phi))
+        res["residual_equals_oracle"] = r1 == ref_res
+    return res
+
+
+def main():
+    names = [a for a in sys.argv[1:] if a.startswith("C")] or ["C1", "C2", "C3", "C4", "C5"]
+    torch.cuda.set_device(0)
+    for n in names:
+        t0 = time.time()
+        res = gsrb_config("--oracle" in sys.argv) if n == "C4" else heat_config(n)
+        res["wall_s"] = time.time() - t0
+        print(json.dumps(res), flush=True)
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
