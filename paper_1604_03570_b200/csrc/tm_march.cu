@@ -357,11 +357,10 @@ int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArg
         if (rows <= 32) return launch_march_one<2, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
         return launch_march_one<2, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     }
-    if (cpl == 4) {
-        if (rows <= 8) return launch_march_one<4, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<4, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<4, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<4, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp
+        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     }
     if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
@@ -404,7 +403,8 @@ int tm_march_plan_create(const tm_block *cols, int64_t ncols, int32_t nctas, tm_
         my = std::max(my, k.ny);
         even = even && (k.x0 % 2 == 0) && (k.nx % 2 == 0);
     }
-    if (mx > 128 || my > 64) return fail(TM_ERR_INVALID, "tm_march_plan_create: column exceeds 128 x 64");
+    if (mx > 128 || my > 64 || (mx > 64 && my > 32))
+        return fail(TM_ERR_INVALID, "tm_march_plan_create: column exceeds 64 x 64 / 128 x 32");
     // equal contiguous shares of the column planes (reference partition rule, iterator.py:93-103)
     std::vector<Segment> segs;
     std::vector<int32_t> begin(nctas + 1, 0);

@@ -49,14 +49,20 @@ def _even_chunks(n: int, cap: int) -> list:
     return out
 
 
-DEFAULT_ROWS = 16  # measured best on C2 (tools/march_perf.py, profiles/march_r01.txt)
+CELLS_PER_PLANE = 1024  # column rows x width per CTA plane; C2 optimum (16 x 64), tools/march_perf.py
+
+
+def warps_for(nx: int, rows: int) -> int:
+    """Consumer warps of the march kernel instance (mirrors launch_march)."""
+    if nx > 64:
+        return 8 if rows <= 8 else 16
+    return 4 if rows <= 8 else (8 if rows <= 32 else 16)
 
 
 def max_rows_for(nx: int, packed: bool) -> int:
     width = nx if packed else nx + 4
     per_stage = SMEM_BUDGET // STAGES // 8 - (2 * 64 if packed else 0)
-    rows = per_stage // width - 2
-    rows = min(DEFAULT_ROWS, rows)
+    rows = min(per_stage // width - 2, max(2, CELLS_PER_PLANE // nx), 64 if nx <= 64 else 32)
     return max(2, rows - rows % 2)
 
 
@@ -106,7 +112,7 @@ def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool) -> int:
     width = nx if packed else nx + 4
     stage = -(-(width * (ny + 2)) // 16) * 16 + (-(-2 * ny // 16) * 16 if packed else 0)
     smem = STAGES * stage * 8 + 128
-    threads = 32 + {8: 128, 16: 256, 32: 256, 64: 512}[min(k for k in (8, 16, 32, 64) if ny <= k)]
+    threads = 32 * (1 + warps_for(nx, ny))
     return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 100)))
 
 

@@ -14,6 +14,9 @@ from tools.sweep_shapes import graph_time  # noqa: E402
 def main():
     cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "C2"
     w = tm.CONFIGS[cfg]
+    if "--scaled" in sys.argv:
+        k = sys.argv.index("--scaled")
+        w = w.scaled(int(sys.argv[k + 1]), int(sys.argv[k + 2]))
     geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
     ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
     a = tm.MultiFab(ba, w.ncomp, w.nghost)
@@ -22,7 +25,7 @@ def main():
     p = tm.HeatParams.stable(1.0, geom.dx)
     cells = w.cells * w.ncomp
     nsm = march.sm_count(a.device)
-    for rows in (None, 32, 16):
+    for rows in (() if "--fused-only" in sys.argv else (None, 32, 16)):
         for mult in (None, 1, 2, 3):
             nctas = None if mult is None else nsm * mult
             try:
@@ -34,7 +37,7 @@ def main():
             print(f"{cfg} march-std rows={rows} nctas={pl.nctas} cols={pl.ncolumns}: {ms * 1e3:.1f} us "
                   f"{16 * cells / ms / 1e6:.0f} GB/s alg ({cells / ms / 1e6:.1f} G cell/s)")
     for rows in (None, 32, 16, 8):
-        for mult in (None, 2, 3, 4):
+        for mult in ((None,) if "--fused-only" in sys.argv else (None, 2, 3, 4)):
             nctas = None if mult is None else nsm * mult
             try:
                 fh = march.FusedHalo(a, b, geom, rows, nctas)
