@@ -218,21 +218,24 @@ class FusedHalo:
         self._init_plan = self._xh_init_plan(a, table)
 
     def _xh_init_plan(self, mf: MultiFab, table) -> "_native.CopyPlan":
-        L = mf.layout
-        tags = np.zeros(2 * len(mf.local_units), dtype=_native.COPY_TAG_DTYPE)
-        slot_unit = {s: u for u, s in mf.slot_of.items()}
-        k = 0
-        for s, u in enumerate(mf.local_units):
-            v = mf.units[u].valid
-            nx, ny, nz = v.extents
-            for side in (0, 1):
-                nb = slot_unit[int(table[s, side])]
-                nv = mf.units[nb].valid
-                col = nv.hi[0] if side == 0 else nv.lo[0]  # left halo <- left neighbour's last column
-                src = cell_offsets(mf, np.array([nb]), np.array([[col, nv.lo[1], nv.lo[2]]]))[0]
-                dst = ((s * mf.ncomp) * self.nzv * 2 + side) * self.nyv
-                tags[k] = (dst, src, 1, ny, nz, 0)
-                k += 1
+        """Copy tags: each slot's two packed x halos <- the x-neighbours'
+        boundary columns (valid y, z range, all components)."""
+        n = len(mf.local_units)
+        slot_unit = np.array(mf.local_units, dtype=np.int64)
+        vlo = np.array([mf.units[u].valid.lo for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
+        vhi = np.array([mf.units[u].valid.hi for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
+        ext = vhi - vlo + 1
+        tags = np.zeros(2 * n, dtype=_native.COPY_TAG_DTYPE)
+        for side in (0, 1):
+            nb_slot = table[:, side].astype(np.int64)
+            cells = vlo[nb_slot].copy()
+            # left halo <- left neighbour's last column; right halo <- right neighbour's first
+            cells[:, 0] = vhi[nb_slot, 0] if side == 0 else vlo[nb_slot, 0]
+            src = cell_offsets(mf, slot_unit[nb_slot], cells)
+            dst = ((np.arange(n, dtype=np.int64) * mf.ncomp) * self.nzv * 2 + side) * self.nyv
+            t = tags[side::2]
+            t["dst_off"], t["src_off"] = dst, src
+            t["ex"], t["ey"], t["ez"] = 1, ext[:, 1], ext[:, 2]
         self.xh_side = (1, 2 * self.nyv, 2 * self.nyv * self.nzv)
         return _native.CopyPlan(tags, mf.ncomp)
 

@@ -443,10 +443,20 @@ def cell_offsets(mf: MultiFab, units: np.ndarray, cells: np.ndarray) -> np.ndarr
     """Element offsets in ``mf.data`` of global cells ``cells`` (n, 3) of
     units ``units`` (component 0)."""
     L = mf.layout
-    vlo = np.array([mf.units[u].valid.lo for u in range(len(mf.units))], dtype=np.int64).reshape(-1, 3)
-    slot = np.full(len(mf.units), -1, dtype=np.int64)
-    for u, s in mf.slot_of.items():
-        slot[u] = s
+    tables = getattr(mf, "_unit_tables", None)
+    if tables is None:  # per-MultiFab cache: valid lo corner and slot of every unit
+        vlo = np.array([mf.units[u].valid.lo for u in range(len(mf.units))], dtype=np.int64).reshape(-1, 3)
+        slot = np.full(len(mf.units), -1, dtype=np.int64)
+        for u, sl in mf.slot_of.items():
+            slot[u] = sl
+        tables = (vlo, slot)
+        try:
+            mf._unit_tables = tables
+        except AttributeError:
+            pass
+    vlo, slot = tables
+    units = np.asarray(units, dtype=np.int64)
+    cells = np.asarray(cells, dtype=np.int64).reshape(-1, 3)
     s = slot[units]
     if np.any(s < 0):
         raise ValueError("cell offsets requested for a unit this rank does not own")
