@@ -146,6 +146,14 @@ int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uo
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, void *stream);
 
+/* Fused red (0) / black (1) Gauss-Seidel pass of the column march, in place on
+ * phi (ncomp 1), x halos from the packed buffer xh, and the updated colour's
+ * boundary values scattered into the face neighbours' halos (phi ghost
+ * rows/planes and xh): the FillBoundary that follows each colour in
+ * BASELINE config 4 is fused.  Same per-cell form as tm_gsrb_color. */
+int tm_gsrb_march(tm_march_plan *plan, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,
+                  const double *rhs, int32_t color, double h2, double *xh, const int32_t *d_nbr, void *stream);
+
 /* ---- reductions (one block per unit, blocks in grid order) --------------- */
 /* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =
  * serial sum of the partials in block order: bit-identical to the

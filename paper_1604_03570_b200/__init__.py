@@ -25,6 +25,7 @@ from .multifab import CONTIGUOUS, REGIONAL, DeviceFab, FillBoundary, MultiFab, f
 from .stencil import (
     HeatParams,
     gsrb_color,
+    gsrb_solve,
     gsrb_sweep,
     heat_amplification,
     heat_step,
@@ -39,7 +40,7 @@ __all__ = [
     "CopyTag", "FillPlan", "build_fill_plan", "shift_candidates", "split_tags",
     "DEFAULT_TILE_SIZE", "MFIter", "TileCursor", "TileSchedule", "build_schedule", "parallel_for_tiles",
     "CONTIGUOUS", "REGIONAL", "DeviceFab", "FillBoundary", "MultiFab", "fill_boundary",
-    "HeatParams", "gsrb_color", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
+    "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
     "residual_maxnorm",
 ]
 

@@ -317,6 +317,231 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Fused red-black Gauss-Seidel colour pass on the same column march.
+//
+// In place on phi: a pass updates only cells of one colour, and every value it
+// reads (x/y/z neighbours) has the other colour, so no CTA ever reads a value
+// another CTA writes in the same pass -- including the halo rows/planes of
+// neighbouring columns and the ghosts it scatters into (colour-c values into
+// ghost cells that this pass reads only at colour 1-c).  Each lane stores its
+// cell pair with double2 (the unchanged cell re-written with the bits it
+// already holds).  The stage holds [phi plane + y halo][packed x halo][rhs rows].
+// Per-cell form (builder-owned, oracle/tm_oracle.c orc_gsrb_color):
+//   s = ((((w + e) + s_) + n) + b) + t ;  phi = (s + h2*rhs) / 6
+// ---------------------------------------------------------------------------
+struct GsrbArgs {
+    MarchArgs m;        // columns, segments, phi (out), layout, xh scatter, nbr, box, stage
+    tm_layout R;        // rhs layout
+    int32_t rhs_off;    // offset of the rhs slice inside a stage (doubles)
+    int32_t color;
+    double h2;
+};
+
+template <int CPL, int NWARP, int RPW>
+__global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1))
+gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap xmap,
+                  const __grid_constant__ CUtensorMap rmap, GsrbArgs ga) {
+    using namespace tmk;
+    const MarchArgs &a = ga.m;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double *stages = reinterpret_cast<double *>(smem_raw);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + (size_t)kStages * a.stage_elems * sizeof(double));
+    uint64_t *empty = bars + kStages;
+
+    const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
+    if (s_begin >= s_end) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int bx = a.box_x;
+    const int ny_box = a.box_y - 2;
+    const uint32_t tx_bytes = (uint32_t)((a.box_x * a.box_y + 2 * ny_box + a.box_x * ny_box) * (int)sizeof(double));
+    const int g_ng = a.L.nghost;
+
+    if (tid == 0) {
+        prefetch_tensormap(&map);
+        prefetch_tensormap(&xmap);
+        prefetch_tensormap(&rmap);
+#pragma unroll
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&empty[s], NWARP);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (warp == NWARP) {  // producer
+        if (lane == 0) {
+            int p = 0;
+            for (int s = s_begin; s < s_end; ++s) {
+                const Segment sg = a.segs[s];
+                const tm_block c = a.cols[sg.col];
+                const int w = c.slot;  // ncomp == 1
+                const int n = sg.k1 - sg.k0 + 2;
+                for (int q = 0; q < n; ++q, ++p) {
+                    const int st_i = p % kStages;
+                    if (p >= kStages) mbar_wait(&empty[st_i], ((p / kStages) - 1) & 1);
+                    double *stage = stages + st_i * a.stage_elems;
+                    const int z = c.z0 + sg.k0 - 1 + q;
+                    mbar_arrive_expect_tx(&bars[st_i], tx_bytes);
+                    tma_load_plane(stage, &map, &bars[st_i], c.x0, c.y0 - 1, z, w);
+                    tma_load_plane(stage + a.xh_off, &xmap, &bars[st_i], c.y0 - g_ng, 0, z - g_ng, w);
+                    tma_load_plane(stage + ga.rhs_off, &rmap, &bars[st_i], c.x0 - a.L.xoff + ga.R.xoff,
+                                   c.y0 - g_ng + ga.R.nghost, z - g_ng + ga.R.nghost, w);
+                }
+            }
+        }
+        return;
+    }
+
+    auto release = [&](int g) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[g % kStages]);
+    };
+    auto wait_plane = [&](int g) { mbar_wait(&bars[g % kStages], (g / kStages) & 1); };
+    const Strides st = strides_of(a.L);
+    const double h2 = ga.h2;
+    int g = 0;
+    for (int s = s_begin; s < s_end; ++s) {
+        const Segment sg = a.segs[s];
+        const tm_block c = a.cols[sg.col];
+        const int nyb = a.nyv, nzb = a.nzv;
+        const int32_t *nb = a.nbr + 6 * c.slot;
+        const int zl0 = c.z0 - g_ng + sg.k0;
+        const bool lane_on = lane * CPL < c.nx;
+        const int xc = min(lane * CPL, c.nx - CPL);
+        const uint32_t sbase = smem_u32(stages);
+        const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
+        const uint32_t ystep = (uint32_t)bx * 8u;
+        uint32_t roff[RPW], xlo[RPW], xro[RPW], rof[RPW];
+        bool on[RPW];
+        double *optr[RPW];
+        int yface[RPW], ylv[RPW], par[RPW];
+#pragma unroll
+        for (int i = 0; i < RPW; ++i) {
+            const int r = warp * RPW + i;
+            const int rc = min(r, c.ny - 1);
+            on[i] = lane_on && r < c.ny;
+            roff[i] = (uint32_t)((rc + 1) * bx + xc) * 8u;
+            xlo[i] = (lane == 0) ? (uint32_t)(a.xh_off + rc) * 8u : roff[i] - 8u;
+            xro[i] = (xc + CPL == c.nx) ? (uint32_t)(a.xh_off + ny_box + rc) * 8u : roff[i] + (uint32_t)CPL * 8u;
+            rof[i] = (uint32_t)(ga.rhs_off + rc * bx + xc) * 8u;
+            optr[i] = a.out + (int64_t)c.slot * st.slot + (int64_t)(c.z0 + sg.k0) * st.plane +
+                      (int64_t)(c.y0 + r) * st.row + c.x0 + xc;
+            ylv[i] = c.y0 - g_ng + r;
+            yface[i] = 0;
+            if (on[i] && ylv[i] == 0 && nb[2] >= 0) yface[i] = 1;
+            if (on[i] && ylv[i] == nyb - 1 && nb[3] >= 0) yface[i] = 2;
+            par[i] = (c.parity + xc + r + sg.k0) & 1;  // colour of cell j=0 of this row at plane k0
+        }
+        const int64_t ydl = (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
+        const int64_t ydh = (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
+        double *xhl = nullptr, *xhr = nullptr;
+        const int xl0 = c.x0 - a.L.xoff + xc;
+        if (lane_on && xl0 == 0 && nb[0] >= 0) xhl = a.xh_new + ((int64_t)(nb[0] * nzb + zl0) * 2 + 1) * nyb;
+        if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0) xhr = a.xh_new + ((int64_t)(nb[1] * nzb + zl0) * 2 + 0) * nyb;
+        const int nk = sg.k1 - sg.k0;
+        int kz_lo = -1, kz_hi = -1;
+        int64_t zoff_lo = 0, zoff_hi = 0;
+        if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
+            kz_lo = -zl0;
+            zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
+        }
+        if (nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
+            kz_hi = nzb - 1 - zl0;
+            zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
+        }
+
+        double um[RPW][CPL], uc[RPW][CPL];
+        wait_plane(g);
+        wait_plane(g + 1);
+        {
+            const uint32_t s0 = sbase + (uint32_t)(g % kStages) * sbytes;
+            const uint32_t s1 = sbase + (uint32_t)((g + 1) % kStages) * sbytes;
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    um[i][j] = lds_f64(s0 + roff[i] + 8u * j);
+                    uc[i][j] = lds_f64(s1 + roff[i] + 8u * j);
+                }
+        }
+        release(g);
+        for (int kk = 0; kk < nk; ++kk) {
+            const int gc = g + 1 + kk, gn = g + 2 + kk;
+            const uint32_t sc = sbase + (uint32_t)(gc % kStages) * sbytes;
+            const uint32_t sn = sbase + (uint32_t)(gn % kStages) * sbytes;
+            wait_plane(gn);
+            double out[RPW][CPL], un[RPW][CPL];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const uint32_t cp = sc + roff[i];
+                double ym[CPL], yp[CPL], rh[CPL];
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    ym[j] = lds_f64(cp - ystep + 8u * j);
+                    yp[j] = lds_f64(cp + ystep + 8u * j);
+                    un[i][j] = lds_f64(sn + roff[i] + 8u * j);
+                    rh[j] = lds_f64(sc + rof[i] + 8u * j);
+                }
+                const double xl = lds_f64(sc + xlo[i]);
+                const double xr = lds_f64(sc + xro[i]);
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    const double w_ = j == 0 ? xl : uc[i][j - 1];
+                    const double e_ = j == CPL - 1 ? xr : uc[i][j + 1];
+                    double sum = rn_add(w_, e_);
+                    sum = rn_add(sum, ym[j]);
+                    sum = rn_add(sum, yp[j]);
+                    sum = rn_add(sum, um[i][j]);
+                    sum = rn_add(sum, un[i][j]);
+                    const double upd = __ddiv_rn(rn_add(sum, rn_mul(h2, rh[j])), 6.0);
+                    out[i][j] = (((par[i] + j + kk) & 1) == ga.color) ? upd : uc[i][j];
+                }
+            }
+            release(gc);
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (!on[i]) continue;
+                double *o = optr[i] + (int64_t)kk * st.plane;
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    if constexpr (CPL >= 2)
+                        *reinterpret_cast<double2 *>(o + j) = make_double2(out[i][j], out[i][j + 1]);
+                    else
+                        o[j] = out[i][j];
+                }
+                double *yo = yface[i] == 0 ? nullptr : o + (yface[i] == 1 ? ydl : ydh);
+                double *zo = kk == kz_lo ? o + zoff_lo : (kk == kz_hi ? o + zoff_hi : nullptr);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    double *d = t == 0 ? yo : zo;
+                    if (!d) continue;
+#pragma unroll
+                    for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                        if constexpr (CPL >= 2)
+                            *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
+                        else
+                            d[j] = out[i][j];
+                    }
+                }
+                if (xhl) xhl[(int64_t)kk * 2 * nyb + ylv[i]] = out[i][0];
+                if (xhr) xhr[(int64_t)kk * 2 * nyb + ylv[i]] = out[i][CPL - 1];
+            }
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    um[i][j] = out[i][j];  // the plane as it is now (z-1 of the next plane)
+                    uc[i][j] = un[i][j];
+                }
+        }
+        release(g + nk + 1);
+        g += nk + 2;
+    }
+}
+
 }  // namespace
 
 struct tm_march_plan {
@@ -366,6 +591,42 @@ int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArg
     if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     return launch_march_one<1, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+}
+
+
+template <int CPL, int NWARP, int RPW>
+int launch_gsrb_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const GsrbArgs &a,
+                    int nctas, size_t smem, cudaStream_t s) {
+    auto kern = gsrb_march_kernel<CPL, NWARP, RPW>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(gsrb march)");
+        configured = true;
+    }
+    kern<<<nctas, (NWARP + 1) * 32, smem, s>>>(map, xmap, rmap, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return tmk::cuda_fail(e, "gsrb march launch");
+    return TM_OK;
+}
+
+int launch_gsrb(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const GsrbArgs &a, int cpl,
+                int rows, int nctas, size_t smem, cudaStream_t s) {
+    if (cpl == 2) {
+        if (rows <= 8) return launch_gsrb_one<2, 4, 2>(map, xmap, rmap, a, nctas, smem, s);
+        if (rows <= 16) return launch_gsrb_one<2, 8, 2>(map, xmap, rmap, a, nctas, smem, s);
+        if (rows <= 32) return launch_gsrb_one<2, 8, 4>(map, xmap, rmap, a, nctas, smem, s);
+        return launch_gsrb_one<2, 16, 4>(map, xmap, rmap, a, nctas, smem, s);
+    }
+    if (cpl == 4) {
+        if (rows <= 8) return launch_gsrb_one<4, 8, 1>(map, xmap, rmap, a, nctas, smem, s);
+        if (rows <= 16) return launch_gsrb_one<4, 16, 1>(map, xmap, rmap, a, nctas, smem, s);
+        return launch_gsrb_one<4, 16, 2>(map, xmap, rmap, a, nctas, smem, s);
+    }
+    if (rows <= 8) return launch_gsrb_one<1, 4, 2>(map, xmap, rmap, a, nctas, smem, s);
+    if (rows <= 16) return launch_gsrb_one<1, 8, 2>(map, xmap, rmap, a, nctas, smem, s);
+    if (rows <= 32) return launch_gsrb_one<1, 8, 4>(map, xmap, rmap, a, nctas, smem, s);
+    return launch_gsrb_one<1, 16, 4>(map, xmap, rmap, a, nctas, smem, s);
 }
 
 int encode_xh_map(CUtensorMap *map, const tm_layout &L, const double *xh, int box_y) {
@@ -513,6 +774,53 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (!packed) return launch_march<false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
     if (!scatter) return launch_march<true, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
     return launch_march<true, true>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+}
+
+int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,
+                  const double *rhs, int32_t color, double h2, double *xh, const int32_t *d_nbr, void *stream) {
+    using namespace tmk;
+    if (!p) return fail(TM_ERR_INVALID, "tm_gsrb_march: null plan");
+    int rc = check_layout(phi_layout, "tm_gsrb_march");
+    if (rc) return rc;
+    rc = check_layout(rhs_layout, "tm_gsrb_march(rhs)");
+    if (rc) return rc;
+    const tm_layout &L = *phi_layout;
+    if (L.nghost < 1 || L.ncomp != 1 || rhs_layout->ncomp != 1 || !phi || !rhs || !xh || !d_nbr ||
+        (color != 0 && color != 1))
+        return fail(TM_ERR_INVALID, "tm_gsrb_march: bad arguments");
+    if (p->ncols == 0) return TM_OK;
+    if (!p->even || p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_gsrb_march: columns must be even-sized");
+    GsrbArgs ga{};
+    MarchArgs &a = ga.m;
+    a.cols = p->d_cols;
+    a.segs = p->d_segs;
+    a.seg_begin = p->d_seg_begin;
+    a.out = phi;
+    a.L = L;
+    a.box_x = p->max_nx;
+    a.box_y = p->max_ny + 2;
+    a.nyv = L.ny - 2 * L.nghost;
+    a.nzv = L.nz - 2 * L.nghost;
+    a.xh_off = ((a.box_x * a.box_y + 15) / 16) * 16;
+    ga.rhs_off = a.xh_off + ((2 * p->max_ny + 15) / 16) * 16;
+    a.stage_elems = ga.rhs_off + ((p->max_nx * p->max_ny + 15) / 16) * 16;
+    a.xh_new = xh;
+    a.nbr = d_nbr;
+    ga.R = *rhs_layout;
+    ga.color = color;
+    ga.h2 = h2;
+    const size_t smem = (size_t)kStages * a.stage_elems * sizeof(double) + 2 * kStages * sizeof(uint64_t);
+    if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_gsrb_march: column plane too large for shared memory");
+    CUtensorMap map, xmap, rmap;
+    rc = encode_plane_map(&map, L, phi, a.box_x, a.box_y);
+    if (rc) return rc;
+    rc = encode_xh_map(&xmap, L, xh, p->max_ny);
+    if (rc) return rc;
+    rc = encode_plane_map(&rmap, *rhs_layout, rhs, p->max_nx, p->max_ny);
+    if (rc) return rc;
+    const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
+    if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_gsrb_march: widths > 64 must be multiples of 4");
+    return launch_gsrb(map, xmap, rmap, ga, cpl, p->max_ny, p->nctas, smem, as_stream(stream));
 }
 
 }  // extern "C"

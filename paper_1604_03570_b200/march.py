@@ -106,23 +106,25 @@ def march_columns(mf: MultiFab, max_rows: int | None = None, packed: bool = Fals
     return out
 
 
-def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool) -> int:
+def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool, rhs_rows: bool = False) -> int:
     nx = int(columns["nx"].max())
     ny = int(columns["ny"].max())
     width = nx if packed else nx + 4
     stage = -(-(width * (ny + 2)) // 16) * 16 + (-(-2 * ny // 16) * 16 if packed else 0)
+    if rhs_rows:  # GSRB stages also carry the column's rhs rows
+        stage += -(-(nx * ny) // 16) * 16
     smem = STAGES * stage * 8 + 128
     threads = 32 * (1 + warps_for(nx, ny))
     return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 100)))
 
 
 def march_plan(mf: MultiFab, packed: bool = False, max_rows: int | None = None,
-               nctas: int | None = None) -> "_native.MarchPlan":
-    key = ("march", packed, max_rows, nctas, mf.layout, tuple(mf.local_units))
+               nctas: int | None = None, rhs_rows: bool = False) -> "_native.MarchPlan":
+    key = ("march", packed, max_rows, nctas, rhs_rows, mf.layout, tuple(mf.local_units))
     plan = mf._plans.get(key)
     if plan is None:
         cols = march_columns(mf, max_rows, packed)
-        n = nctas or sm_count(mf.device) * ctas_per_sm(mf, cols, packed)
+        n = nctas or sm_count(mf.device) * ctas_per_sm(mf, cols, packed, rhs_rows)
         plan = _native.MarchPlan(cols, n)
         mf._plans[key] = plan
     return plan
@@ -195,6 +197,29 @@ def fusable(mf: MultiFab, geom: Geometry) -> bool:
     return face_neighbors(mf, geom) is not None
 
 
+def xh_init_plan(mf: MultiFab, table, nyv: int, nzv: int):
+    """Copy tags: each slot's two packed x halos <- the x-neighbours'
+    boundary columns (valid y, z range, all components).  Returns
+    (CopyPlan, packed-halo side strides)."""
+    n = len(mf.local_units)
+    slot_unit = np.array(mf.local_units, dtype=np.int64)
+    vlo = np.array([mf.units[u].valid.lo for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
+    vhi = np.array([mf.units[u].valid.hi for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
+    ext = vhi - vlo + 1
+    tags = np.zeros(2 * n, dtype=_native.COPY_TAG_DTYPE)
+    for side in (0, 1):
+        nb_slot = table[:, side].astype(np.int64)
+        cells = vlo[nb_slot].copy()
+        # left halo <- left neighbour's last column; right halo <- right neighbour's first
+        cells[:, 0] = vhi[nb_slot, 0] if side == 0 else vlo[nb_slot, 0]
+        src = cell_offsets(mf, slot_unit[nb_slot], cells)
+        dst = ((np.arange(n, dtype=np.int64) * mf.ncomp) * nzv * 2 + side) * nyv
+        t = tags[side::2]
+        t["dst_off"], t["src_off"] = dst, src
+        t["ex"], t["ey"], t["ez"] = 1, ext[:, 1], ext[:, 2]
+    return _native.CopyPlan(tags, mf.ncomp), (1, 2 * nyv, 2 * nyv * nzv)
+
+
 class FusedHalo:
     """Packed x halos + neighbour table shared by an old/new MultiFab pair."""
 
@@ -218,26 +243,8 @@ class FusedHalo:
         self._init_plan = self._xh_init_plan(a, table)
 
     def _xh_init_plan(self, mf: MultiFab, table) -> "_native.CopyPlan":
-        """Copy tags: each slot's two packed x halos <- the x-neighbours'
-        boundary columns (valid y, z range, all components)."""
-        n = len(mf.local_units)
-        slot_unit = np.array(mf.local_units, dtype=np.int64)
-        vlo = np.array([mf.units[u].valid.lo for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
-        vhi = np.array([mf.units[u].valid.hi for u in mf.local_units], dtype=np.int64).reshape(-1, 3)
-        ext = vhi - vlo + 1
-        tags = np.zeros(2 * n, dtype=_native.COPY_TAG_DTYPE)
-        for side in (0, 1):
-            nb_slot = table[:, side].astype(np.int64)
-            cells = vlo[nb_slot].copy()
-            # left halo <- left neighbour's last column; right halo <- right neighbour's first
-            cells[:, 0] = vhi[nb_slot, 0] if side == 0 else vlo[nb_slot, 0]
-            src = cell_offsets(mf, slot_unit[nb_slot], cells)
-            dst = ((np.arange(n, dtype=np.int64) * mf.ncomp) * self.nzv * 2 + side) * self.nyv
-            t = tags[side::2]
-            t["dst_off"], t["src_off"] = dst, src
-            t["ex"], t["ey"], t["ez"] = 1, ext[:, 1], ext[:, 2]
-        self.xh_side = (1, 2 * self.nyv, 2 * self.nyv * self.nzv)
-        return _native.CopyPlan(tags, mf.ncomp)
+        plan, self.xh_side = xh_init_plan(mf, table, self.nyv, self.nzv)
+        return plan
 
     def prime(self, mf: MultiFab, plan=None) -> None:
         """Fill every halo of ``mf`` from its valid data (regular FillBoundary
@@ -256,3 +263,50 @@ class FusedHalo:
             self.plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
             self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), old.stream()),
             "tm_heat_march(fused)")
+
+
+class FusedGSRB:
+    """Red-black Gauss-Seidel sweeps as two fused launches per sweep (red
+    pass + halo scatter, black pass + halo scatter), in place on ``phi``.
+    Bit-identical to ``stencil.gsrb_sweep`` (red, FillBoundary, black,
+    FillBoundary)."""
+
+    def __init__(self, phi: MultiFab, rhs: MultiFab, geom: Geometry, max_rows: int | None = None,
+                 nctas: int | None = None):
+        import torch
+
+        if not fusable(phi, geom) or phi.ncomp != 1 or rhs.ncomp != 1:
+            raise ValueError("layout is not eligible for the fused GSRB path")
+        if phi.ba != rhs.ba or phi.local_units != rhs.local_units:
+            raise ValueError("phi and rhs must share the BoxArray and distribution")
+        self.phi, self.rhs, self.geom = phi, rhs, geom
+        L = phi.layout
+        self.nyv = L.ny - 2 * L.nghost
+        self.nzv = L.nz - 2 * L.nghost
+        self.xh = torch.zeros((L.nslots, self.nzv, 2, self.nyv), dtype=torch.float64, device=phi.device)
+        table = face_neighbors(phi, geom)
+        self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=phi.device)
+        self.plan = march_plan(phi, True, max_rows, nctas, rhs_rows=True)
+        self._init, self.xh_side = xh_init_plan(phi, table, self.nyv, self.nzv)
+        self.h2 = geom.dx[0] * geom.dx[0]
+
+    def prime(self, plan=None) -> None:
+        from .multifab import fill_boundary
+
+        fill_boundary(self.phi, self.geom, plan)
+        self._init.run(self.xh.data_ptr(), self.xh_side, self.phi.ptr, self.phi.layout.side(), self.phi.stream())
+
+    def colour(self, color: int) -> None:
+        phi, rhs = self.phi, self.rhs
+        _native.check(_native.load().tm_gsrb_march(
+            self.plan.handle, phi.layout.to_c(), phi.ptr, rhs.layout.to_c(), rhs.ptr, color, self.h2,
+            self.xh.data_ptr(), self.nbr.data_ptr(), phi.stream()), "tm_gsrb_march")
+
+    def sweep(self) -> None:
+        self.colour(0)
+        self.colour(1)
+
+    def finalize(self, plan=None) -> None:
+        from .multifab import fill_boundary
+
+        fill_boundary(self.phi, self.geom, plan)

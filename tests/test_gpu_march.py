@@ -109,3 +109,25 @@ def test_fusable_rules(tm):
     uneven = tm.Box((0, 0, 0), (59, 63, 63))
     assert not fusable(tm.MultiFab(tm.BoxArray.chop(uneven, 24), 1, 1), tm.Geometry(uneven))
     assert not fusable(tm.MultiFab(tm.BoxArray.chop(dom, 32), 1, 0), geom)
+
+
+@pytest.mark.parametrize("n,mgs,sweeps,rows", [(64, 32, 5, None), (64, 32, 4, 8), (32, 16, 6, None),
+                                               (128, 64, 3, None)])
+def test_fused_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
+    w = tm.CONFIGS["C4"].scaled(n, mgs, sweeps)
+    rhs_g = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    phi = tm.MultiFab(ba, 1, 1)
+    rhs = tm.MultiFab(ba, 1, 0)
+    rhs.from_global(rhs_g)
+    tm.gsrb_solve(phi, rhs, geom, sweeps, fused=True, max_rows=rows)
+    ref_phi, ref_res = orc.gsrb_periodic(np.zeros((n,) * 3), rhs_g[0], sweeps, w.dx * w.dx)
+    assert np.array_equal(phi.to_global().cpu().numpy()[0], ref_phi)
+    assert tm.residual_maxnorm(phi, rhs, geom) == ref_res
+    # a second solve continues from the current state, fused == unfused
+    phi2 = tm.MultiFab(ba, 1, 1)
+    phi2.data.copy_(phi.data)
+    tm.gsrb_solve(phi, rhs, geom, 2, fused=True, max_rows=rows)
+    tm.gsrb_solve(phi2, rhs, geom, 2, fused=False)
+    assert np.array_equal(phi.to_global().cpu().numpy(), phi2.to_global().cpu().numpy())

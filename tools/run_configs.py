@@ -90,13 +90,23 @@ def gsrb_config(oracle: bool):
     rhs.from_global(rhs_g)
     plan = tm.build_fill_plan(phi, geom)
     sched = tm.build_schedule(phi, w.tile_size)
-    tm.gsrb_sweep(phi, rhs, geom, sched, plan)  # warm
+    tm.gsrb_solve(phi, rhs, geom, 1, sched, plan, fused=True)  # warm (plans, halo tables)
+    tm.gsrb_sweep(phi, rhs, geom, sched, plan)
     phi.fill(0.0)
     r0 = tm.residual_maxnorm(phi, rhs, geom, sched)
-    secs = ev_time(lambda: [tm.gsrb_sweep(phi, rhs, geom, sched, plan) for _ in range(w.steps)])
-    r1 = tm.residual_maxnorm(phi, rhs, geom, sched)
-    res = {"config": "C4", "cells": w.cells, "sweeps": w.steps, "rate": w.cells * w.steps / secs,
-           "ms_per_sweep": secs / w.steps * 1e3, "residual0": r0, "residual": r1, "residual_decreased": r1 < r0}
+    res = {"config": "C4", "cells": w.cells, "sweeps": w.steps, "residual0": r0}
+    finals = {}
+    for fused in (True, False):
+        phi.fill(0.0)
+        secs = ev_time(lambda: tm.gsrb_solve(phi, rhs, geom, w.steps, sched, plan, fused=fused))
+        key = "fused" if fused else "unfused"
+        res[key + "_rate"] = w.cells * w.steps / secs
+        res[key + "_ms_per_sweep"] = secs / w.steps * 1e3
+        res[key + "_residual"] = tm.residual_maxnorm(phi, rhs, geom, sched)
+        finals[key] = phi.to_global()
+    res["fused_equals_unfused"] = bool(torch.equal(finals["fused"], finals["unfused"]))
+    r1 = res["fused_residual"]
+    res["residual_decreased"] = r1 < r0
     if oracle:
         from oracle import oracle as orc
 
