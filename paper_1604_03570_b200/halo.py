@@ -95,6 +95,11 @@ class HaloExchange:
                 arr["ex"], arr["ey"], arr["ez"] = ext[:, 0], ext[:, 1], ext[:, 2]
             return arr, spans, off
 
+        # ghost boxes of local units that only a remote rank can fill (for overlap splitting)
+        self.remote_dst: dict = {}
+        for ids in recvs.values():
+            for n in ids:
+                self.remote_dst.setdefault(tags[n][0], []).append(tags[n][1])
         pack_tags, self.send_spans, nsend = build(sends, True)
         unpack_tags, self.recv_spans, nrecv = build(recvs, False)
         self.pack = _native.CopyPlan(pack_tags, nc)

@@ -587,3 +587,35 @@ def schedule_sweep_plan(mf: MultiFab, schedule: TileSchedule, zmerge: bool = Fal
         plan = _native.SweepPlan(sweep_blocks(mf, schedule.entries, zmerge))
         schedule._device[key] = plan
     return plan
+
+
+def split_blocks(mf: MultiFab, blocks: np.ndarray, remote_dst: dict):
+    """Split sweep blocks into (interior, boundary): a block is boundary when
+    the 7-point stencil of one of its cells can touch a ghost cell that only
+    a remote rank fills.  Interior blocks can run while the halo messages
+    are in flight."""
+    from .box import intersect as _isect
+
+    L = mf.layout
+    inner, outer = [], []
+    for b in blocks:
+        u = mf.local_units[int(b["slot"])]
+        v = mf.units[u].valid
+        lo = (v.lo[0] + int(b["x0"]) - L.xoff - 1, v.lo[1] + int(b["y0"]) - L.nghost - 1,
+              v.lo[2] + int(b["z0"]) - L.nghost - 1)
+        grown = Box(lo, (lo[0] + int(b["nx"]) + 1, lo[1] + int(b["ny"]) + 1, lo[2] + int(b["nz"]) + 1))
+        hit = any(not _isect(grown, rb).is_empty for rb in remote_dst.get(u, ()))
+        (outer if hit else inner).append(b)
+    mk = lambda rows: np.array(rows, dtype=_native.BLOCK_DTYPE) if rows else np.zeros(0, dtype=_native.BLOCK_DTYPE)
+    return mk(inner), mk(outer)
+
+
+def overlap_sweep_plans(mf: MultiFab, schedule: TileSchedule, remote_dst: dict, zmerge: bool = False):
+    """(interior, boundary) SweepPlans of a schedule for halo/compute overlap."""
+    key = ("overlap", mf.layout, tuple(mf.local_units), zmerge, mf.rank, mf.dm.nranks)
+    plans = schedule._device.get(key)
+    if plans is None:
+        inner, outer = split_blocks(mf, sweep_blocks(mf, schedule.entries, zmerge), remote_dst)
+        plans = (_native.SweepPlan(inner), _native.SweepPlan(outer))
+        schedule._device[key] = plans
+    return plans

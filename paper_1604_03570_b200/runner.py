@@ -19,7 +19,9 @@ Two step implementations, bit-identical in the valid cells:
   regular FillBoundary at the end of ``advance``, so the MultiFab handed
   back has every ghost filled.
 
-Multi-rank runs (NCCL halo exchange) step eagerly with ``fused=False``.
+Multi-rank runs (NCCL halo exchange) step eagerly with ``fused=False``: the
+interior tiles are swept while the halo messages are in flight
+(``stencil.overlapped_step``).
 """
 
 from __future__ import annotations
@@ -28,7 +30,7 @@ from .boxarray import Geometry
 from .fillplan import FillPlan, build_fill_plan
 from .mfiter import TileSchedule, build_schedule
 from .multifab import MultiFab, comm_info, fill_boundary
-from .stencil import HeatParams, heat_step
+from .stencil import HeatParams, heat_step, overlapped_step
 
 
 class HeatRunner:
@@ -75,6 +77,8 @@ class HeatRunner:
     def _step(self, old: MultiFab, new: MultiFab) -> None:
         if self.fused:
             self.fh.step(new, old, self.params)
+        elif old.dm.nranks > 1:  # halo messages overlap the interior sweep
+            overlapped_step(new, old, self.geom, self.params, self.plan, self.schedule, self.zmerge)
         else:
             fill_boundary(old, self.geom, self.plan)
             heat_step(new, old, self.geom, self.params, self.schedule, zmerge=self.zmerge)

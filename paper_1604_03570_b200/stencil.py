@@ -89,6 +89,40 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
                                   dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
 
 
+def heat_sweep_plan(mf_new: MultiFab, mf_old: MultiFab, params: HeatParams, plan) -> None:
+    """Kernel A over an explicit block table (e.g. the interior or boundary
+    half of an overlapped step).  No checks: internal helper."""
+    if plan.nblocks == 0:
+        return
+    dxi0, dxi1, dxi2, dtD = params.coefficients()
+    _native.check(_native.load().tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr, 0,
+                                               mf_old.ncomp, dxi0, dxi1, dxi2, dtD, mf_old.stream()),
+                  "tm_heat_sweep")
+
+
+def overlapped_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatParams, plan,
+                    schedule: TileSchedule, zmerge: bool = False) -> None:
+    """FillBoundary + heat sweep with the remote halo exchange overlapped:
+    pack and post the NCCL sends/receives, run the intra-GPU copies and the
+    sweep of every tile whose stencil cannot see a remote ghost, then wait
+    for the messages, unpack and sweep the remaining (boundary) tiles.
+    Results are identical to fill_boundary + heat_step."""
+    from .multifab import _device_fill, overlap_sweep_plans
+
+    copy, halo = _device_fill(mf_old, plan)
+    stream = mf_old.stream()
+    if halo is None:
+        copy.run(mf_old.ptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
+        heat_step(mf_new, mf_old, geom, params, schedule, zmerge=zmerge)
+        return
+    inner, outer = overlap_sweep_plans(mf_old, schedule, halo.remote_dst, zmerge)
+    halo.start(stream)
+    copy.run(mf_old.ptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
+    heat_sweep_plan(mf_new, mf_old, params, inner)
+    halo.finish(stream)
+    heat_sweep_plan(mf_new, mf_old, params, outer)
+
+
 def _check_poisson(phi: MultiFab, rhs: MultiFab):
     if phi.nghost < 1:
         raise ValueError("GSRB requires nghost >= 1 on phi")
