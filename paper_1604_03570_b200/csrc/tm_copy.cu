@@ -164,6 +164,8 @@ int tm_copy_plan_create(const tm_copy_tag *tags, int64_t ntags, int32_t ncomp, t
 
 int tm_copy_plan_destroy(tm_copy_plan *plan) {
     if (!plan) return TM_OK;
+    // tables may still be read by queued launches on any stream: drain before freeing
+    cudaDeviceSynchronize();
     cudaFree(plan->d_tags);
     cudaFree(plan->d_prefix);
     cudaFree(plan->d_items);

@@ -714,6 +714,8 @@ int tm_march_plan_create(const tm_block *cols, int64_t ncols, int32_t nctas, tm_
 
 int tm_march_plan_destroy(tm_march_plan *p) {
     if (!p) return TM_OK;
+    // tables may still be read by queued launches on any stream: drain before freeing
+    cudaDeviceSynchronize();
     cudaFree(p->d_cols);
     cudaFree(p->d_segs);
     cudaFree(p->d_seg_begin);

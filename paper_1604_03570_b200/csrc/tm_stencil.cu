@@ -485,6 +485,8 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
 
 int tm_sweep_plan_destroy(tm_sweep_plan *plan) {
     if (!plan) return TM_OK;
+    // tables may still be read by queued launches on any stream: drain before freeing
+    cudaDeviceSynchronize();
     cudaFree(plan->d_blocks);
     delete plan;
     return TM_OK;

@@ -73,7 +73,7 @@ class HaloExchange:
 
         from .multifab import cell_offsets
 
-        self.mf = mf
+        self.device = mf.device
         tags = plan.tags
         _, sends, recvs = exchange_lists(mf.dm.owners, tags, mf.rank)
         nc = mf.ncomp
@@ -110,22 +110,36 @@ class HaloExchange:
         self.bytes_recv = nrecv * 8
         self._reqs = None
 
-    def start(self, stream: int) -> None:
+    def start(self, mf, stream: int) -> None:
+        """Pack every outgoing message of ``mf`` (one launch) and post the
+        grouped sends/receives.  NCCL orders them after the pack on the
+        current stream; ``finish`` makes the stream wait for the receives.
+        The exchange object is shared by every MultiFab of the same layout
+        (e.g. both buffers of a double-buffered pair), so the field is
+        passed per call."""
+        import torch
         import torch.distributed as dist
 
-        mf = self.mf
         packed = (0, 0, 0)
         self.pack.run(self.sendbuf.data_ptr(), packed, mf.ptr, mf.layout.side(), stream)
+        self._host = dist.get_backend() == "gloo"
+        if self._host:  # CPU transport (tests): stage through host memory
+            torch.cuda.current_stream(self.device).synchronize()
+            sbuf = self.sendbuf.cpu()
+            self._hrecv = torch.empty(self.recvbuf.shape, dtype=torch.float64)
+        else:
+            sbuf, self._hrecv = self.sendbuf, self.recvbuf
         ops = []
         for peer, off, n in self.send_spans:
-            ops.append(dist.P2POp(dist.isend, self.sendbuf[off:off + n], peer))
+            ops.append(dist.P2POp(dist.isend, sbuf[off:off + n], peer))
         for peer, off, n in self.recv_spans:
-            ops.append(dist.P2POp(dist.irecv, self.recvbuf[off:off + n], peer))
+            ops.append(dist.P2POp(dist.irecv, self._hrecv[off:off + n], peer))
         self._reqs = dist.batch_isend_irecv(ops) if ops else []
 
-    def finish(self, stream: int) -> None:
+    def finish(self, mf, stream: int) -> None:
         for r in self._reqs or []:
             r.wait()
         self._reqs = None
-        mf = self.mf
+        if self._host:
+            self.recvbuf.copy_(self._hrecv)
         self.unpack.run(mf.ptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)

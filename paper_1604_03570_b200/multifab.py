@@ -513,10 +513,10 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
     copy, halo = _device_fill(mf, plan)
     stream = mf.stream()
     if halo is not None:
-        halo.start(stream)
+        halo.start(mf, stream)
     copy.run(mf.ptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
     if halo is not None:
-        halo.finish(stream)
+        halo.finish(mf, stream)
 
 
 FillBoundary = fill_boundary

@@ -116,10 +116,10 @@ def overlapped_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: 
         heat_step(mf_new, mf_old, geom, params, schedule, zmerge=zmerge)
         return
     inner, outer = overlap_sweep_plans(mf_old, schedule, halo.remote_dst, zmerge)
-    halo.start(stream)
+    halo.start(mf_old, stream)
     copy.run(mf_old.ptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
     heat_sweep_plan(mf_new, mf_old, params, inner)
-    halo.finish(stream)
+    halo.finish(mf_old, stream)
     heat_sweep_plan(mf_new, mf_old, params, outer)
 
 

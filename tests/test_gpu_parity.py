@@ -373,8 +373,9 @@ def test_overlap_split_is_a_partition_and_exact(tm):
     tm.fill_boundary(one, geom)
     a, b = one.clone_empty(), one.clone_empty()
     p = tm.HeatParams.stable(1.0, geom.dx)
-    tm.heat_step(a, one, geom, p, sched)
-    blocks1 = sweep_blocks(one, sched.entries)
+    sched1 = tm.build_schedule(one, w.tile_size)
+    tm.heat_step(a, one, geom, p, sched1)
+    blocks1 = sweep_blocks(one, sched1.entries)
     fake_remote = {u: [bx for bx in halo.remote_dst.get(u, [])] for u in range(len(ba))}
     i1, o1 = split_blocks(one, blocks1, fake_remote)
     heat_sweep_plan(b, one, p, _native.SweepPlan(i1))
