@@ -224,9 +224,16 @@ def run_ours(args, w):
     from paper_1604_03570_b200.runner import HeatRunner
 
     rank, world, local = dist_env()
+    # one process per GPU; TM_DIST_BACKEND=gloo lets several ranks share one GPU to
+    # smoke-test the multi-rank path (host-staged halos) -- never used for numbers
+    backend = os.environ.get("TM_DIST_BACKEND", "nccl")
+    local = local % torch.cuda.device_count() if backend == "gloo" else local
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
 
     def barrier():
