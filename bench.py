@@ -348,7 +348,7 @@ def run_ours(args, w):
             rate, cores, sample, _, _, _ = cpu_reference_rate(w, args.cpu_seconds)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
         traffic = profile_traffic(w.name, runner.fused)
-        launches_per_step = runner.launches_per_step + (2 if world > 1 else 0)
+        launches_per_step = runner.launches_per_step
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,

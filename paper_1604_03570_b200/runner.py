@@ -67,7 +67,10 @@ class HeatRunner:
 
     @property
     def launches_per_step(self) -> int:
-        return 1 if self.fused else 2
+        if self.fused:
+            return 1
+        # multi-rank: pack, local copies, interior sweep, unpack, boundary sweep
+        return 5 if self.a.dm.nranks > 1 else 2
 
     def reset(self) -> None:
         """Call after modifying ``a`` from outside: restart at step 0."""
