@@ -127,84 +127,106 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     }
 
     // ---------------- consumer warps ----------------
-    auto release = [&](int g) {
+    // Hot-loop bookkeeping is kept to 32-bit offsets and running counters: the
+    // plane loop is issue-bound as much as it is memory-bound (ncu: ~60% issue
+    // active), so every per-plane integer instruction costs time.
+    const uint32_t sbase = smem_u32(stages);
+    const uint32_t bfull = smem_u32(bars), bempty = smem_u32(empty);
+    const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
+    auto saddr = [&](uint32_t q) { return sbase + (q & (kStages - 1)) * sbytes; };
+    auto wait_plane = [&](uint32_t q) { mbar_wait_u32(bfull + (q & (kStages - 1)) * 8u, (q / kStages) & 1u); };
+    auto release = [&](uint32_t q) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[g % kStages]);
+        if (lane == 0) mbar_arrive_u32(bempty + (q & (kStages - 1)) * 8u);
     };
-    auto wait_plane = [&](int g) { mbar_wait(&bars[g % kStages], (g / kStages) & 1); };
 
     const double c0 = a.c0, c1 = a.c1, c2 = a.c2, c3 = a.c3;
     const Strides st = strides_of(a.L);
     const int g_ng = a.L.nghost;
     const int xsh = PACKED ? 0 : 2;  // smem column of a column's first cell (x0 is even)
-    int g = 0;                       // global plane index of the current segment's first plane
+    const int max_ny = a.box_y - 2;
+    const uint32_t ystep = (uint32_t)bx * 8u;
+    const uint32_t pstep = (uint32_t)st.plane;  // < 2^31 (host-checked)
+    const int nyb = a.nyv, nzb = a.nzv;
+    uint32_t g = 0;  // CTA-wide plane counter of the current segment's first plane
 
     for (int s = s_begin; s < s_end; ++s) {
         const Segment sg = a.segs[s];
         const tm_block c = a.cols[sg.col];
+        const int nk = sg.k1 - sg.k0;
+        const int xi = min(lane * CPL, c.nx - CPL);  // lane's first cell (clamped for idle lanes)
         const bool lane_on = lane * CPL < c.nx;
-        int ci[RPW];
+        // output rows: 64-bit row bases + one 32-bit running plane offset
+        double *const obase = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp;
+        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + xi);
+        double *orow[RPW];
         bool on[RPW];
-        double *optr[RPW];
-        // SCATTER targets hoisted out of the k loop (null = this row/lane has no face there)
-        // y faces: at most one row per column has yl == 0 (-y face) or yl == nyb-1 (+y face);
-        // its neighbour ghost row is o + ydelta.  x faces: the lane holding x = 0 / x = nx-1
-        // writes into the neighbour's packed halo at xh_base + yl (+ xstep per plane).
-        int yface[RPW];  // 0 none, 1 -y, 2 +y
-        int ylv[RPW];
-        int64_t ydl = 0, ydh = 0;
-        double *xhl = nullptr, *xhr = nullptr;
-        const int64_t obase = (int64_t)c.slot * st.slot + (int64_t)comp * st.comp +
-                              (int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + lane * CPL;
-        const int nyb = a.nyv, nzb = a.nzv;
-        const int32_t *nb = a.nbr + 6 * c.slot;
-        const int zl0 = c.z0 - g_ng + sg.k0;  // valid z index of the segment's first plane
+        uint32_t roff[RPW];  // smem byte offset of the row's first cell (rows past max_ny clamp; never stored)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = warp * RPW + i;
             on[i] = lane_on && r < c.ny;
-            ci[i] = (min(r, c.ny - 1) + 1) * bx + min(lane * CPL, c.nx - CPL) + xsh;
-            optr[i] = a.out + obase + (int64_t)r * st.row;
-            yface[i] = 0;
-            ylv[i] = c.y0 - g_ng + r;
-            if (SCATTER && on[i]) {
-                if (ylv[i] == 0 && nb[2] >= 0) yface[i] = 1;
-                if (ylv[i] == nyb - 1 && nb[3] >= 0) yface[i] = 2;
-            }
+            orow[i] = obase + (int64_t)r * st.row;
+            roff[i] = (uint32_t)((min(r, max_ny) + 1) * bx + xi + xsh) * 8u;
         }
-        if (SCATTER) {
-            ydl = (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
-            ydh = (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
-            const int xl0 = c.x0 - a.L.xoff + lane * CPL;
-            if (lane_on && xl0 == 0 && nb[0] >= 0)  // our x=0 column -> the -x neighbour's right halo
-                xhl = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb;
-            if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0)
-                xhr = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb;
-        }
-        // ---- per-segment invariants: shared-memory byte offsets of this lane's operands ----
-        const uint32_t sbase = smem_u32(stages);
-        const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
-        const uint32_t ystep = (uint32_t)bx * 8u;
-        uint32_t roff[RPW], xlo[RPW], xro[RPW];
+        uint32_t xlo[RPW], xro[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = min(warp * RPW + i, c.ny - 1);
-            roff[i] = (uint32_t)ci[i] * 8u;
             const bool left_edge = PACKED && lane == 0;
-            const bool right_edge = PACKED && (min(lane * CPL, c.nx - CPL) + CPL == c.nx);
+            const bool right_edge = PACKED && (xi + CPL == c.nx);
             xlo[i] = left_edge ? (uint32_t)(a.xh_off + r) * 8u : roff[i] - 8u;
-            xro[i] = right_edge ? (uint32_t)(a.xh_off + (a.box_y - 2) + r) * 8u : roff[i] + (uint32_t)CPL * 8u;
+            xro[i] = right_edge ? (uint32_t)(a.xh_off + max_ny + r) * 8u : roff[i] + (uint32_t)CPL * 8u;
         }
-        const int64_t pstep = st.plane;  // doubles per plane (output pointers)
-        const int64_t xstep = 2 * (int64_t)nyb;
+        // SCATTER targets.  y: only the column's first row (-y face) and last row (+y face)
+        // can be box faces; z: two planes of the column, warp-uniform; x: the lanes holding
+        // x = 0 / x = nx-1 write the neighbour's packed halo (consecutive y, one plane apart).
+        const int32_t *nb = a.nbr + 6 * c.slot;
+        const int zl0 = c.z0 - g_ng + sg.k0;  // valid z index of the segment's first plane
+        const int yl0 = c.y0 - g_ng;          // valid y index of the column's first row
+        int ylo_i = -1, yhi_i = -1;
+        double *ylo = nullptr, *yhi = nullptr;
+        double *xhp = nullptr;
+        bool x_right = false;
+        int kz_lo = -1, kz_hi = -1;
+        int64_t zoff_lo = 0, zoff_hi = 0;
+        if (SCATTER) {
+            if (warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
+                ylo_i = 0;
+                ylo = orow[0] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
+            }
+            const int rl = c.ny - 1;  // last row of the column
+            if (yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
+                yhi_i = rl % RPW;
+                yhi = obase + (int64_t)rl * st.row + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
+            }
+            const int xl0 = c.x0 - a.L.xoff + lane * CPL;
+            if (lane_on && xl0 == 0 && nb[0] >= 0)  // our x = 0 cells -> the -x neighbour's right halo
+                xhp = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb + yl0 +
+                      warp * RPW;
+            if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0) {
+                xhp = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb + yl0 +
+                      warp * RPW;
+                x_right = true;
+            }
+            if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
+                kz_lo = -zl0;
+                zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
+            }
+            if (nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
+                kz_hi = nzb - 1 - zl0;
+                zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
+            }
+        }
+        const uint32_t xstep = 2u * (uint32_t)nyb;
+        uint32_t xk = 0;
 
         // priming: planes k0-1 and k0 -> carried z flux and centre values
         double ua[RPW][CPL], ub[RPW][CPL], fzm[RPW][CPL];
         wait_plane(g);
         wait_plane(g + 1);
         {
-            const uint32_t s0 = sbase + (uint32_t)(g % kStages) * sbytes;
-            const uint32_t s1 = sbase + (uint32_t)((g + 1) % kStages) * sbytes;
+            const uint32_t s0 = saddr(g), s1 = saddr(g + 1);
 #pragma unroll
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
@@ -215,42 +237,42 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 }
         }
         release(g);
-        const int nk = sg.k1 - sg.k0;
-        // z faces: plane index (within the segment) whose values go to a z neighbour's ghost plane
-        int kz_lo = -1, kz_hi = -1;
-        int64_t zoff_lo = 0, zoff_hi = 0;
-        if (SCATTER) {
-            if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
-                kz_lo = -zl0;
-                zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
-            }
-            if (nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
-                kz_hi = nzb - 1 - zl0;
-                zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
-            }
-        }
         // one plane: centre values in cur, next-plane values land in nxt
         auto plane = [&](int kk, double (&cur)[RPW][CPL], double (&nxt)[RPW][CPL]) {
-            const int gc = g + 1 + kk, gn = g + 2 + kk;
-            const uint32_t sc = sbase + (uint32_t)(gc % kStages) * sbytes;
-            const uint32_t sn = sbase + (uint32_t)(gn % kStages) * sbytes;
-            wait_plane(gn);
-            double out[RPW][CPL];
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
+            const uint32_t gc = g + 1 + (uint32_t)kk;
+            const uint32_t sc = saddr(gc), sn = saddr(gc + 1);
+            wait_plane(gc + 1);
+            // y fluxes between consecutive rows are shared by the two rows (same bits)
+            double fy[RPW + 1][CPL];
+            {
                 double ym[CPL], yp[CPL];
-                const uint32_t cp = sc + roff[i];
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2) {
-                        lds_f64x2(cp - ystep + 8u * j, ym[j], ym[j + 1]);
-                        lds_f64x2(cp + ystep + 8u * j, yp[j], yp[j + 1]);
-                        lds_f64x2(sn + roff[i] + 8u * j, nxt[i][j], nxt[i][j + 1]);
+                        lds_f64x2(sc + roff[0] - ystep + 8u * j, ym[j], ym[j + 1]);
+                        lds_f64x2(sc + roff[RPW - 1] + ystep + 8u * j, yp[j], yp[j + 1]);
                     } else {
-                        ym[j] = lds_f64(cp - ystep + 8u * j);
-                        yp[j] = lds_f64(cp + ystep + 8u * j);
-                        nxt[i][j] = lds_f64(sn + roff[i] + 8u * j);
+                        ym[j] = lds_f64(sc + roff[0] - ystep + 8u * j);
+                        yp[j] = lds_f64(sc + roff[RPW - 1] + ystep + 8u * j);
                     }
+                }
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) {
+                    fy[0][j] = rn_mul(rn_sub(cur[0][j], ym[j]), c1);
+#pragma unroll
+                    for (int i = 1; i < RPW; ++i) fy[i][j] = rn_mul(rn_sub(cur[i][j], cur[i - 1][j]), c1);
+                    fy[RPW][j] = rn_mul(rn_sub(yp[j], cur[RPW - 1][j]), c1);
+                }
+            }
+            double out[RPW][CPL];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    if constexpr (CPL >= 2)
+                        lds_f64x2(sn + roff[i] + 8u * j, nxt[i][j], nxt[i][j + 1]);
+                    else
+                        nxt[i][j] = lds_f64(sn + roff[i] + 8u * j);
                 }
                 const double xl = lds_f64(sc + xlo[i]);
                 const double xr = lds_f64(sc + xro[i]);
@@ -262,9 +284,8 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
                     const double u0 = cur[i][j];
-                    const double fym = rn_mul(rn_sub(u0, ym[j]), c1), fyp = rn_mul(rn_sub(yp[j], u0), c1);
                     const double fzp = rn_mul(rn_sub(nxt[i][j], u0), c2);
-                    double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fyp, fym), c1));
+                    double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
                     sum = rn_add(sum, rn_mul(rn_sub(fzp, fzm[i][j]), c2));
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
                     fzm[i][j] = fzp;
@@ -272,39 +293,39 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
             }
             // all shared reads of the centre plane are done: hand its stage back early
             release(gc);
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                if (!on[i]) continue;
-                double *o = optr[i];
+            auto st_cells = [&](double *d, int i) {
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2)
-                        *reinterpret_cast<double2 *>(o + j) = make_double2(out[i][j], out[i][j + 1]);
+                        *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
                     else
-                        o[j] = out[i][j];
+                        d[j] = out[i][j];
                 }
+            };
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (!on[i]) continue;
+                st_cells(orow[i] + koff, i);
                 if (SCATTER) {
-                    double *zo = nullptr;
-                    if (kk == kz_lo) zo = o + zoff_lo;
-                    if (kk == kz_hi) zo = o + zoff_hi;
-                    double *yo = yface[i] == 0 ? nullptr : o + (yface[i] == 1 ? ydl : ydh);
-#pragma unroll
-                    for (int t = 0; t < 2; ++t) {
-                        double *d = t == 0 ? yo : zo;
-                        if (!d) continue;
-#pragma unroll
-                        for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
-                            if constexpr (CPL >= 2)
-                                *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
-                            else
-                                d[j] = out[i][j];
-                        }
-                    }
-                    if (xhl) xhl[(int64_t)kk * xstep + ylv[i]] = out[i][0];
-                    if (xhr) xhr[(int64_t)kk * xstep + ylv[i]] = out[i][CPL - 1];
+                    if (i == ylo_i) st_cells(ylo + koff, i);
+                    if (i == yhi_i) st_cells(yhi + koff, i);
                 }
-                optr[i] += pstep;
             }
+            if (SCATTER) {
+                if (kk == kz_lo || kk == kz_hi) {  // warp-uniform, two planes per column
+                    const int64_t zd = kk == kz_lo ? zoff_lo : zoff_hi;
+#pragma unroll
+                    for (int i = 0; i < RPW; ++i)
+                        if (on[i]) st_cells(orow[i] + koff + zd, i);
+                }
+                if (xhp) {
+#pragma unroll
+                    for (int i = 0; i < RPW; ++i)
+                        if (on[i]) xhp[xk + i] = x_right ? out[i][CPL - 1] : out[i][0];
+                }
+                xk += xstep;
+            }
+            koff += pstep;
         };
         int kk = 0;
         for (; kk + 1 < nk; kk += 2) {  // ping-pong: no register rotation
@@ -734,6 +755,8 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (L.nghost < 1 || !uold || !unew || uold == unew)
         return fail(TM_ERR_INVALID, "tm_heat_march: needs nghost >= 1 and distinct old/new fields");
     if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march: bad ncomp");
+    if (strides_of(L).comp >= ((int64_t)1 << 32))
+        return fail(TM_ERR_INVALID, "tm_heat_march: one component of a slot must hold < 2^32 doubles");
     const bool packed = xh_old != nullptr;
     const bool scatter = xh_new != nullptr;
     if (scatter && (!packed || !d_nbr)) return fail(TM_ERR_INVALID, "tm_heat_march: scatter needs xh_old and nbr");
