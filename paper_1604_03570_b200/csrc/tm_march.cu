@@ -416,53 +416,70 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
         return;
     }
 
-    auto release = [&](int g) {
+    const uint32_t sbase = smem_u32(stages);
+    const uint32_t bfull = smem_u32(bars), bempty = smem_u32(empty);
+    const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
+    auto saddr = [&](uint32_t q) { return sbase + (q & (kStages - 1)) * sbytes; };
+    auto wait_plane = [&](uint32_t q) { mbar_wait_u32(bfull + (q & (kStages - 1)) * 8u, (q / kStages) & 1u); };
+    auto release = [&](uint32_t q) {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[g % kStages]);
+        if (lane == 0) mbar_arrive_u32(bempty + (q & (kStages - 1)) * 8u);
     };
-    auto wait_plane = [&](int g) { mbar_wait(&bars[g % kStages], (g / kStages) & 1); };
     const Strides st = strides_of(a.L);
     const double h2 = ga.h2;
-    int g = 0;
+    const uint32_t ystep = (uint32_t)bx * 8u;
+    const uint32_t pstep = (uint32_t)st.plane;  // < 2^31 (host-checked)
+    const int nyb = a.nyv, nzb = a.nzv;
+    uint32_t g = 0;
     for (int s = s_begin; s < s_end; ++s) {
         const Segment sg = a.segs[s];
         const tm_block c = a.cols[sg.col];
-        const int nyb = a.nyv, nzb = a.nzv;
+        const int nk = sg.k1 - sg.k0;
         const int32_t *nb = a.nbr + 6 * c.slot;
         const int zl0 = c.z0 - g_ng + sg.k0;
+        const int yl0 = c.y0 - g_ng;
         const bool lane_on = lane * CPL < c.nx;
         const int xc = min(lane * CPL, c.nx - CPL);
-        const uint32_t sbase = smem_u32(stages);
-        const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
-        const uint32_t ystep = (uint32_t)bx * 8u;
+        double *const obase = a.out + (int64_t)c.slot * st.slot;  // ncomp == 1
+        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + xc);
         uint32_t roff[RPW], xlo[RPW], xro[RPW], rof[RPW];
         bool on[RPW];
-        double *optr[RPW];
-        int yface[RPW], ylv[RPW], par[RPW];
+        double *orow[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = warp * RPW + i;
             const int rc = min(r, c.ny - 1);
             on[i] = lane_on && r < c.ny;
-            roff[i] = (uint32_t)((rc + 1) * bx + xc) * 8u;
+            orow[i] = obase + (int64_t)r * st.row;
+            roff[i] = (uint32_t)((min(r, ny_box) + 1) * bx + xc) * 8u;  // rows past ny_box clamp; never stored
             xlo[i] = (lane == 0) ? (uint32_t)(a.xh_off + rc) * 8u : roff[i] - 8u;
             xro[i] = (xc + CPL == c.nx) ? (uint32_t)(a.xh_off + ny_box + rc) * 8u : roff[i] + (uint32_t)CPL * 8u;
-            rof[i] = (uint32_t)(ga.rhs_off + rc * bx + xc) * 8u;
-            optr[i] = a.out + (int64_t)c.slot * st.slot + (int64_t)(c.z0 + sg.k0) * st.plane +
-                      (int64_t)(c.y0 + r) * st.row + c.x0 + xc;
-            ylv[i] = c.y0 - g_ng + r;
-            yface[i] = 0;
-            if (on[i] && ylv[i] == 0 && nb[2] >= 0) yface[i] = 1;
-            if (on[i] && ylv[i] == nyb - 1 && nb[3] >= 0) yface[i] = 2;
-            par[i] = (c.parity + xc + r + sg.k0) & 1;  // colour of cell j=0 of this row at plane k0
+            rof[i] = (uint32_t)(ga.rhs_off + min(r, ny_box - 1) * bx + xc) * 8u;
         }
-        const int64_t ydl = (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
-        const int64_t ydh = (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
-        double *xhl = nullptr, *xhr = nullptr;
+        // colour of this lane's cell 0 in row 0 at plane k0, flipped per row and per plane
+        const int par0 = (c.parity + xc + warp * RPW + sg.k0 + ga.color) & 1;
+        // scatter targets (see march_kernel)
+        int ylo_i = -1, yhi_i = -1;
+        double *ylo = nullptr, *yhi = nullptr, *xhp = nullptr;
+        bool x_right = false;
+        if (warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
+            ylo_i = 0;
+            ylo = orow[0] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
+        }
+        {
+            const int rl = c.ny - 1;
+            if (yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
+                yhi_i = rl % RPW;
+                yhi = obase + (int64_t)rl * st.row + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
+            }
+        }
         const int xl0 = c.x0 - a.L.xoff + xc;
-        if (lane_on && xl0 == 0 && nb[0] >= 0) xhl = a.xh_new + ((int64_t)(nb[0] * nzb + zl0) * 2 + 1) * nyb;
-        if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0) xhr = a.xh_new + ((int64_t)(nb[1] * nzb + zl0) * 2 + 0) * nyb;
-        const int nk = sg.k1 - sg.k0;
+        if (lane_on && xl0 == 0 && nb[0] >= 0)
+            xhp = a.xh_new + ((int64_t)(nb[0] * nzb + zl0) * 2 + 1) * nyb + yl0 + warp * RPW;
+        if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0) {
+            xhp = a.xh_new + ((int64_t)(nb[1] * nzb + zl0) * 2 + 0) * nyb + yl0 + warp * RPW;
+            x_right = true;
+        }
         int kz_lo = -1, kz_hi = -1;
         int64_t zoff_lo = 0, zoff_hi = 0;
         if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
@@ -473,13 +490,14 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
             kz_hi = nzb - 1 - zl0;
             zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
         }
+        const uint32_t xstep = 2u * (uint32_t)nyb;
+        uint32_t xk = 0;
 
         double um[RPW][CPL], uc[RPW][CPL];
         wait_plane(g);
         wait_plane(g + 1);
         {
-            const uint32_t s0 = sbase + (uint32_t)(g % kStages) * sbytes;
-            const uint32_t s1 = sbase + (uint32_t)((g + 1) % kStages) * sbytes;
+            const uint32_t s0 = saddr(g), s1 = saddr(g + 1);
 #pragma unroll
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
@@ -490,66 +508,85 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
         }
         release(g);
         for (int kk = 0; kk < nk; ++kk) {
-            const int gc = g + 1 + kk, gn = g + 2 + kk;
-            const uint32_t sc = sbase + (uint32_t)(gc % kStages) * sbytes;
-            const uint32_t sn = sbase + (uint32_t)(gn % kStages) * sbytes;
-            wait_plane(gn);
+            const uint32_t gc = g + 1 + (uint32_t)kk;
+            const uint32_t sc = saddr(gc), sn = saddr(gc + 1);
+            wait_plane(gc + 1);
             double out[RPW][CPL], un[RPW][CPL];
 #pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                const uint32_t cp = sc + roff[i];
-                double ym[CPL], yp[CPL], rh[CPL];
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    ym[j] = lds_f64(cp - ystep + 8u * j);
-                    yp[j] = lds_f64(cp + ystep + 8u * j);
-                    un[i][j] = lds_f64(sn + roff[i] + 8u * j);
-                    rh[j] = lds_f64(sc + rof[i] + 8u * j);
-                }
-                const double xl = lds_f64(sc + xlo[i]);
-                const double xr = lds_f64(sc + xro[i]);
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    const double w_ = j == 0 ? xl : uc[i][j - 1];
-                    const double e_ = j == CPL - 1 ? xr : uc[i][j + 1];
-                    double sum = rn_add(w_, e_);
-                    sum = rn_add(sum, ym[j]);
-                    sum = rn_add(sum, yp[j]);
-                    sum = rn_add(sum, um[i][j]);
-                    sum = rn_add(sum, un[i][j]);
-                    const double upd = __ddiv_rn(rn_add(sum, rn_mul(h2, rh[j])), 6.0);
-                    out[i][j] = (((par[i] + j + kk) & 1) == ga.color) ? upd : uc[i][j];
-                }
-            }
-            release(gc);
-#pragma unroll
-            for (int i = 0; i < RPW; ++i) {
-                if (!on[i]) continue;
-                double *o = optr[i] + (int64_t)kk * st.plane;
+            for (int i = 0; i < RPW; ++i)
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2)
-                        *reinterpret_cast<double2 *>(o + j) = make_double2(out[i][j], out[i][j + 1]);
+                        lds_f64x2(sn + roff[i] + 8u * j, un[i][j], un[i][j + 1]);
                     else
-                        o[j] = out[i][j];
+                        un[i][j] = lds_f64(sn + roff[i] + 8u * j);
                 }
-                double *yo = yface[i] == 0 ? nullptr : o + (yface[i] == 1 ? ydl : ydh);
-                double *zo = kk == kz_lo ? o + zoff_lo : (kk == kz_hi ? o + zoff_hi : nullptr);
 #pragma unroll
-                for (int t = 0; t < 2; ++t) {
-                    double *d = t == 0 ? yo : zo;
-                    if (!d) continue;
+            for (int i = 0; i < RPW; ++i) {
+                // p: offset of the updated cell inside each cell pair (CPL >= 2); for CPL == 1
+                // the lane's single cell is updated iff p == 0.  Neighbours x+-1 of an updated
+                // cell are this lane's other-colour cells or the row's x halo.
+                const int p = (par0 + i + kk) & 1;
+                if constexpr (CPL == 1) {
+                    const double xl = lds_f64(sc + xlo[i]), xr = lds_f64(sc + xro[i]);
+                    const double ym = i > 0 ? uc[i - 1][0] : lds_f64(sc + roff[0] - ystep);
+                    const double yp = i < RPW - 1 ? uc[i + 1][0] : lds_f64(sc + roff[RPW - 1] + ystep);
+                    const double rh = lds_f64(sc + rof[i]);
+                    double sum = rn_add(rn_add(rn_add(rn_add(rn_add(xl, xr), ym), yp), um[i][0]), un[i][0]);
+                    const double upd = __ddiv_rn(rn_add(sum, rn_mul(h2, rh)), 6.0);
+                    out[i][0] = p == 0 ? upd : uc[i][0];
+                } else {
+                    const double xe = lds_f64(sc + (p ? xro[i] : xlo[i]));  // the one x halo value needed
 #pragma unroll
-                    for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
-                        if constexpr (CPL >= 2)
-                            *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
-                        else
-                            d[j] = out[i][j];
+                    for (int jp = 0; jp < CPL / 2; ++jp) {
+                        const int j0 = 2 * jp;
+                        const uint32_t jb = 8u * (uint32_t)(j0 + p);
+                        const double w_ = p ? uc[i][j0] : (jp == 0 ? xe : uc[i][j0 - 1]);
+                        const double e_ = p ? (jp == CPL / 2 - 1 ? xe : uc[i][j0 + 2]) : uc[i][j0 + 1];
+                        const double ym = i > 0 ? (p ? uc[i - 1][j0 + 1] : uc[i - 1][j0])
+                                                : lds_f64(sc + roff[0] - ystep + jb);
+                        const double yp = i < RPW - 1 ? (p ? uc[i + 1][j0 + 1] : uc[i + 1][j0])
+                                                      : lds_f64(sc + roff[RPW - 1] + ystep + jb);
+                        const double zm = p ? um[i][j0 + 1] : um[i][j0];
+                        const double zp = p ? un[i][j0 + 1] : un[i][j0];
+                        const double rh = lds_f64(sc + rof[i] + jb);
+                        double sum = rn_add(rn_add(rn_add(rn_add(rn_add(w_, e_), ym), yp), zm), zp);
+                        const double upd = __ddiv_rn(rn_add(sum, rn_mul(h2, rh)), 6.0);
+                        out[i][j0] = p ? uc[i][j0] : upd;
+                        out[i][j0 + 1] = p ? upd : uc[i][j0 + 1];
                     }
                 }
-                if (xhl) xhl[(int64_t)kk * 2 * nyb + ylv[i]] = out[i][0];
-                if (xhr) xhr[(int64_t)kk * 2 * nyb + ylv[i]] = out[i][CPL - 1];
             }
+            release(gc);
+            auto st_cells = [&](double *d, int i) {
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    if constexpr (CPL >= 2)
+                        *reinterpret_cast<double2 *>(d + j) = make_double2(out[i][j], out[i][j + 1]);
+                    else
+                        d[j] = out[i][j];
+                }
+            };
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (!on[i]) continue;
+                st_cells(orow[i] + koff, i);
+                if (i == ylo_i) st_cells(ylo + koff, i);
+                if (i == yhi_i) st_cells(yhi + koff, i);
+            }
+            if (kk == kz_lo || kk == kz_hi) {
+                const int64_t zd = kk == kz_lo ? zoff_lo : zoff_hi;
+#pragma unroll
+                for (int i = 0; i < RPW; ++i)
+                    if (on[i]) st_cells(orow[i] + koff + zd, i);
+            }
+            if (xhp) {
+#pragma unroll
+                for (int i = 0; i < RPW; ++i)
+                    if (on[i]) xhp[xk + i] = x_right ? out[i][CPL - 1] : out[i][0];
+            }
+            xk += xstep;
+            koff += pstep;
 #pragma unroll
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
@@ -815,6 +852,8 @@ int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, co
         return fail(TM_ERR_INVALID, "tm_gsrb_march: bad arguments");
     if (p->ncols == 0) return TM_OK;
     if (!p->even || p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_gsrb_march: columns must be even-sized");
+    if (strides_of(L).comp >= ((int64_t)1 << 32))
+        return fail(TM_ERR_INVALID, "tm_gsrb_march: one slot must hold < 2^32 doubles");
     GsrbArgs ga{};
     MarchArgs &a = ga.m;
     a.cols = p->d_cols;

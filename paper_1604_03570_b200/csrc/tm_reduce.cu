@@ -18,29 +18,66 @@ extern "C" int tm_internal_plan_blocks(const tm_sweep_plan *p, const tm_block **
 
 namespace {
 
-__global__ void __launch_bounds__(32) serial_sum_kernel(const tm_block *__restrict__ blocks, const double *__restrict__ base,
+// The chain of dependent adds is the reference's and cannot be shortened; what
+// must not sit on it is memory or shuffle latency.  Two warps per grid: warp 1
+// gathers the next batch of kBatch cells (flat x-fastest, then y, z order)
+// into a shared-memory double buffer while lane 0 of warp 0 adds the current
+// batch serially, reading ahead with 16-byte shared loads.
+constexpr int kBatch = 1024;
+
+__global__ void __launch_bounds__(64) serial_sum_kernel(const tm_block *__restrict__ blocks, const double *__restrict__ base,
                                                         tm_layout L, int comp, double *__restrict__ partial) {
+    __shared__ __align__(16) double buf[2][kBatch];
     const tm_block b = blocks[blockIdx.x];
     const tmk::Strides st = tmk::strides_of(L);
-    const int lane = threadIdx.x;
-    const double *p0 = base + (int64_t)b.slot * st.slot + (int64_t)comp * st.comp;
-    double total = 0.0;
-    for (int k = 0; k < b.nz; ++k)
-        for (int j = 0; j < b.ny; ++j) {
-            const double *row = p0 + (int64_t)(b.z0 + k) * st.plane + (int64_t)(b.y0 + j) * st.row + b.x0;
-            int x = 0;
-            for (; x + 32 <= b.nx; x += 32) {  // full chunks: shuffles unrolled, only the adds chain
-                const double v = __ldg(row + x + lane);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double *p0 = base + (int64_t)b.slot * st.slot + (int64_t)comp * st.comp +
+                       (int64_t)b.z0 * st.plane + (int64_t)b.y0 * st.row + b.x0;
+    const int64_t n = (int64_t)b.nx * b.ny * b.nz;
+    const int64_t nbatch = (n + kBatch - 1) / kBatch;
+    auto gather = [&](int64_t bi) {  // warp 1 only
+        double *dst = buf[bi & 1];
+        for (int t0 = 0; t0 < kBatch / 32; t0 += 8) {
+            double v[8];
 #pragma unroll
-                for (int l = 0; l < 32; ++l) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, l));
+            for (int u = 0; u < 8; ++u) {
+                const int64_t idx = bi * kBatch + (t0 + u) * 32 + lane;
+                v[u] = 0.0;
+                if (idx < n) {
+                    const int64_t r = idx / b.nx;
+                    const int64_t k = r / b.ny;
+                    v[u] = __ldg(p0 + k * st.plane + (r - k * b.ny) * st.row + (idx - r * b.nx));
+                }
             }
-            if (x < b.nx) {
-                const int n = b.nx - x;
-                const double v = lane < n ? __ldg(row + x + lane) : 0.0;
-                for (int l = 0; l < n; ++l) total = __dadd_rn(total, __shfl_sync(0xffffffffu, v, l));
+#pragma unroll
+            for (int u = 0; u < 8; ++u) dst[(t0 + u) * 32 + lane] = v[u];
+        }
+    };
+    if (warp == 1) gather(0);
+    __syncthreads();
+    double total = 0.0;
+    for (int64_t bi = 0; bi < nbatch; ++bi) {
+        if (warp == 1) {
+            if (bi + 1 < nbatch) gather(bi + 1);
+        } else if (lane == 0) {
+            const uint32_t src = tmk::smem_u32(buf[bi & 1]);
+            const int64_t left = n - bi * kBatch;
+            const int cnt = left < kBatch ? (int)left : kBatch;
+            if (cnt == kBatch) {
+                for (int t = 0; t < kBatch; t += 32) {
+                    double v[32];
+#pragma unroll
+                    for (int u = 0; u < 32; u += 2) tmk::lds_f64x2(src + 8u * (t + u), v[u], v[u + 1]);
+#pragma unroll
+                    for (int u = 0; u < 32; ++u) total = __dadd_rn(total, v[u]);
+                }
+            } else {
+                for (int t = 0; t < cnt; ++t) total = __dadd_rn(total, tmk::lds_f64(src + 8u * t));
             }
         }
-    if (lane == 0) partial[blockIdx.x] = total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partial[blockIdx.x] = total;
 }
 
 __global__ void ordered_sum_kernel(const double *__restrict__ partial, int64_t n, double *__restrict__ out) {
@@ -123,7 +160,7 @@ int tm_reduce_sum(tm_sweep_plan *plan, const tm_layout *layout, const double *ba
     int rc = check_args(plan, layout, base, comp, "tm_reduce_sum", &blocks, &n);
     if (rc) return rc;
     if (!d_partial || !d_total) return fail(TM_ERR_INVALID, "tm_reduce_sum: null output");
-    serial_sum_kernel<<<(unsigned)n, 32, 0, as_stream(stream)>>>(blocks, base, *layout, comp, d_partial);
+    serial_sum_kernel<<<(unsigned)n, 64, 0, as_stream(stream)>>>(blocks, base, *layout, comp, d_partial);
     ordered_sum_kernel<<<1, 1, 0, as_stream(stream)>>>(d_partial, n, d_total);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tm_reduce_sum launch");

@@ -289,6 +289,7 @@ class FusedGSRB:
         self.plan = march_plan(phi, True, max_rows, nctas, rhs_rows=True)
         self._init, self.xh_side = xh_init_plan(phi, table, self.nyv, self.nzv)
         self.h2 = geom.dx[0] * geom.dx[0]
+        self._graph = None
 
     def prime(self, plan=None) -> None:
         from .multifab import fill_boundary
@@ -305,6 +306,32 @@ class FusedGSRB:
     def sweep(self) -> None:
         self.colour(0)
         self.colour(1)
+
+    def run(self, sweeps: int, use_graph: bool = True) -> None:
+        """``sweeps`` sweeps.  A colour pass is tens of microseconds of device
+        time, less than the host cost of issuing it, so after one eager
+        sweep (which also warms the plans) one sweep is captured as a CUDA
+        graph and replayed."""
+        import torch
+
+        k = 0
+        if use_graph and self._graph is None and sweeps >= 2:
+            self.sweep()
+            k = 1
+            cur = torch.cuda.current_stream(self.phi.device)
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream(self.phi.device)
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(g, stream=s):
+                    self.sweep()
+            cur.wait_stream(s)
+            self._graph = g
+        for _ in range(k, sweeps):
+            if use_graph and self._graph is not None:
+                self._graph.replay()
+            else:
+                self.sweep()
 
     def finalize(self, plan=None) -> None:
         from .multifab import fill_boundary

@@ -234,8 +234,7 @@ def gsrb_solve(phi: MultiFab, rhs: MultiFab, geom: Geometry, sweeps: int, schedu
             fg = FusedGSRB(phi, rhs, geom, max_rows)
             phi._plans[key] = fg
         fg.prime(plan)
-        for _ in range(sweeps):
-            fg.sweep()
+        fg.run(sweeps)
         fg.finalize(plan)
         return phi
     for _ in range(sweeps):
