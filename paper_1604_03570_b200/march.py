@@ -26,7 +26,8 @@ from .boxarray import BoxIndex, Geometry
 from .multifab import MultiFab, cell_offsets
 
 SMEM_BUDGET = 220 * 1024
-STAGES = 4
+STAGES = 4        # heat ring depth (tm_march.cu kHeatStages)
+GSRB_STAGES = 4   # GSRB ring depth (kGsrbStages)
 
 
 def sm_count(device) -> int:
@@ -113,7 +114,7 @@ def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool, rhs_rows: bool 
     stage = -(-(width * (ny + 2)) // 16) * 16 + (-(-2 * ny // 16) * 16 if packed else 0)
     if rhs_rows:  # GSRB stages also carry the column's rhs rows
         stage += -(-(nx * ny) // 16) * 16
-    smem = STAGES * stage * 8 + 128
+    smem = (GSRB_STAGES if rhs_rows else STAGES) * stage * 8 + 128
     threads = 32 * (1 + warps_for(nx, ny))
     return max(1, min(228 * 1024 // (smem + 1024), 2048 // threads, 65536 // (threads * 100)))
 
