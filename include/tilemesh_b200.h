@@ -154,6 +154,18 @@ int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uo
 int tm_gsrb_march(tm_march_plan *plan, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,
                   const double *rhs, int32_t color, double h2, double *xh, const int32_t *d_nbr, void *stream);
 
+/* ---- 9-point 8th-order Laplacian step ("wide4", Kernel W) -------------------
+ * Replaces compiled.wide4_tiles / wide4_range (compiled.py:102-141) as driven
+ * by kernels.wide4_step (kernels.py:218-247) and loop_wide4_step
+ * (kernels.py:309-342), over every column of a march plan (columns of the
+ * full box width <= 128, <= 16 rows (<= 8 when wider than 64), full z).
+ * coeffs5 = host array {c0, c1, c2, c3, c4} (StencilCoeffs8); dxi2_d = 1/dx_d^2;
+ * dtD = D*dt.  Needs nghost >= 4 with filled ghosts (FillBoundary).  Per cell,
+ * in the reference's operation order, FMA-free: bit-identical. */
+int tm_wide4_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                   int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                   double dtD, void *stream);
+
 /* ---- reductions (one block per unit, blocks in grid order) --------------- */
 /* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =
  * serial sum of the partials in block order: bit-identical to the

@@ -57,6 +57,9 @@ def lib():
                                      ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                                      ctypes.c_int]
         L.orc_heat_tiles.restype = None
+        L.orc_wide4_tiles.argtypes = [_f64p, _f64p, _i64p, _i64p, _i64p, _i64p, ctypes.c_int64] + \
+            [ctypes.c_double] * 9 + [ctypes.c_int]
+        L.orc_wide4_tiles.restype = None
         L.orc_serial_sum.argtypes = [_f64p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int, _i64p, _i64p]
         L.orc_serial_sum.restype = ctypes.c_double
         L.orc_reduce_sum.argtypes = [_f64p, _i64p, _i64p, _i64p, _i64p, ctypes.c_int64, ctypes.c_int]
@@ -173,6 +176,42 @@ def heat_step(new: HostMF, old: HostMF, tiles, dxi, dtD: float, nthreads: int = 
         lib().orc_heat_tiles(_p(new.buf, _f64p), _p(old.buf, _f64p), _p(off, _i64p), _p(lo, _i64p),
                              _p(ext, _i64p), _p(arr, _i64p), len(arr), c, dxi[0], dxi[1], dxi[2], dtD,
                              nthreads)
+
+
+def wide4_step(new: HostMF, old: HostMF, tiles, coeffs, dxi2, dtD: float, nthreads: int = 1) -> None:
+    """Reference kernels.wide4_step (kernels.py:218-247) over ``tiles`` of
+    component 0, cell form compiled.wide4_range (compiled.py:102-129)."""
+    arr = tiles if isinstance(tiles, np.ndarray) else tiles_array(tiles)
+    arr = np.ascontiguousarray(arr, dtype=np.int64)
+    off, lo, ext = old.tables()
+    c = [float(v) for v in coeffs]
+    lib().orc_wide4_tiles(_p(new.buf, _f64p), _p(old.buf, _f64p), _p(off, _i64p), _p(lo, _i64p), _p(ext, _i64p),
+                          _p(arr, _i64p), len(arr), c[0], c[1], c[2], c[3], c[4], dxi2[0], dxi2[1], dxi2[2], dtD,
+                          nthreads)
+
+
+def wide4_periodic(u: np.ndarray, steps: int, coeffs, dxi2, dtD: float) -> np.ndarray:
+    """Whole-domain numpy form, fully periodic; ``u`` (nz, ny, nx)."""
+    c = [float(v) for v in coeffs]
+    u = np.array(u, dtype=np.float64, copy=True)
+    for _ in range(steps):
+        p = np.pad(u, 4, mode="wrap")
+        n = u.shape
+        core = p[4:4 + n[0], 4:4 + n[1], 4:4 + n[2]]
+
+        def sh(axis, m):
+            sl = [slice(4, 4 + n[0]), slice(4, 4 + n[1]), slice(4, 4 + n[2])]
+            sl[axis] = slice(4 + m, 4 + m + n[axis])
+            return p[tuple(sl)]
+
+        s = []
+        for axis in (2, 1, 0):  # x, y, z
+            acc = c[0] * core
+            for m in range(1, 5):
+                acc = acc + c[m] * (sh(axis, -m) + sh(axis, m))
+            s.append(acc)
+        u = core + dtD * (s[0] * dxi2[0] + s[1] * dxi2[1] + s[2] * dxi2[2])
+    return u
 
 
 def reduce_sum(mf: HostMF, comp: int = 0) -> float:

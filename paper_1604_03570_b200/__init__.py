@@ -4,9 +4,10 @@ Drop-in for the reference package ``tilemesh``
 (/root/reference/pkg/src/tilemesh/__init__.py) on the hot path: the same
 names (Box algebra, BoxArray, Geometry, MultiFab, build_fill_plan,
 fill_boundary, build_schedule, TileCursor, HeatParams, heat_step) plus the
-north-star additions DistributionMapping, MFIter, FillBoundary and the
-GSRB / residual kernels.  Storage lives on the GPU; every data-path
-operation is an sm_100a kernel of libtilemesh_b200.so (no CPU fallback).
+north-star additions DistributionMapping, MFIter, FillBoundary, the GSRB /
+residual kernels and the wide4 (8th-order, 4-ghost) step.  Storage lives on
+the GPU; every data-path operation is an sm_100a kernel of
+libtilemesh_b200.so (no CPU fallback).
 """
 
 from .box import Box, box_diff, decompose, grow, intersect, shift, to_face
@@ -32,6 +33,14 @@ from .stencil import (
     init_cosine,
     residual_maxnorm,
 )
+from .wide4 import (
+    StencilCoeffs8,
+    derive_coeffs8,
+    loop_wide4_step,
+    wide4_amplification,
+    wide4_stable_dt,
+    wide4_step,
+)
 
 __all__ = [
     "Box", "box_diff", "decompose", "grow", "intersect", "shift", "to_face",
@@ -42,6 +51,7 @@ __all__ = [
     "CONTIGUOUS", "REGIONAL", "DeviceFab", "FillBoundary", "MultiFab", "fill_boundary",
     "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
     "residual_maxnorm",
+    "StencilCoeffs8", "derive_coeffs8", "loop_wide4_step", "wide4_amplification", "wide4_stable_dt", "wide4_step",
 ]
 
 __version__ = "0.1.0"

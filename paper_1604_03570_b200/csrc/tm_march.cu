@@ -25,20 +25,16 @@
 #include <string>
 #include <vector>
 
-#include "tm_common.cuh"
+#include "tm_march_plan.cuh"
 
 namespace {
+
+using tmk::Segment;
 
 // TMA ring depth (powers of two: stage and phase come from the plane counter by mask/shift).
 // (8 heat stages measured: C2 62.6 us vs 56.9 us at 4 -- fewer CTAs fit; C3/C5 within +-3 %.)
 constexpr int kHeatStages = 4;
 constexpr int kGsrbStages = 4;
-
-struct Segment {
-    int32_t col;     // column index
-    int32_t k0, k1;  // local planes [k0, k1) of the column
-    int32_t reserved;
-};
 
 struct MarchArgs {
     const tm_block *cols;
@@ -604,16 +600,6 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 }
 
 }  // namespace
-
-struct tm_march_plan {
-    int64_t ncols = 0, nsegs = 0;
-    int32_t nctas = 0;
-    tm_block *d_cols = nullptr;
-    Segment *d_segs = nullptr;
-    int32_t *d_seg_begin = nullptr;
-    int max_nx = 0, max_ny = 0;
-    bool even = true;
-};
 
 namespace {
 

@@ -1,0 +1,25 @@
+// Column/segment tables of the persistent march kernels (tm_march.cu heat and
+// GSRB, tm_wide4.cu): library-internal, shared by the translation units.
+#pragma once
+
+#include "tm_common.cuh"
+
+namespace tmk {
+
+struct Segment {
+    int32_t col;     // column index
+    int32_t k0, k1;  // local planes [k0, k1) of the column
+    int32_t reserved;
+};
+
+}  // namespace tmk
+
+struct tm_march_plan {
+    int64_t ncols = 0, nsegs = 0;
+    int32_t nctas = 0;
+    tm_block *d_cols = nullptr;
+    tmk::Segment *d_segs = nullptr;
+    int32_t *d_seg_begin = nullptr;
+    int max_nx = 0, max_ny = 0;
+    bool even = true;
+};

@@ -251,8 +251,8 @@ class MultiFab:
         for u in self.local_units:
             v = self.units[u].valid
             I, J, K = np.ogrid[v.lo[0]:v.hi[0] + 1, v.lo[1]:v.hi[1] + 1, v.lo[2]:v.hi[2] + 1]
-            vals = np.broadcast_to(np.asarray(fn(I, J, K), dtype=np.float64), v.extents)
-            self.fab(u).view(v, comp, 1)[..., 0].copy_(torch.from_numpy(np.ascontiguousarray(vals)))
+            vals = np.array(np.broadcast_to(np.asarray(fn(I, J, K), dtype=np.float64), v.extents), order="C")
+            self.fab(u).view(v, comp, 1)[..., 0].copy_(torch.from_numpy(vals))
 
     def fill(self, v: float, comp: int | None = None) -> None:
         if comp is None:

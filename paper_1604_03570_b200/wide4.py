@@ -1,0 +1,147 @@
+"""The 9-point 8th-order Laplacian step ("wide4").
+
+Reference: ``StencilCoeffs8`` / ``derive_coeffs8`` (kernels.py:49-83),
+``wide4_step`` (kernels.py:218-247), ``loop_wide4_step`` (kernels.py:309-342),
+``wide4_amplification`` / ``wide4_stable_dt`` (kernels.py:380-404), cell form
+``compiled.wide4_range`` (compiled.py:102-129).
+
+Host code keeps the reference expressions (same dt, dxi2 and coefficient
+bits); the update itself is ONE launch of Kernel W (``tm_wide4_march``,
+csrc/tm_wide4.cu) over every box this rank owns, bit-identical to the
+reference per cell.  It reuses the FillBoundary plan and kernel unchanged:
+callers fill 4 ghost layers first, exactly as with the reference.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .boxarray import Geometry
+from .multifab import MultiFab
+
+RADIUS = 4
+
+
+@dataclass(frozen=True)
+class StencilCoeffs8:
+    """Centred second-derivative weights for offsets 0, +-1 .. +-4."""
+
+    c0: float
+    c1: float
+    c2: float
+    c3: float
+    c4: float
+
+    def as_array(self) -> np.ndarray:
+        return np.array([self.c0, self.c1, self.c2, self.c3, self.c4])
+
+    def weights9(self) -> np.ndarray:
+        c = self.as_array()
+        return np.array([c[4], c[3], c[2], c[1], c[0], c[1], c[2], c[3], c[4]])
+
+
+def derive_coeffs8() -> StencilCoeffs8:
+    """Even Taylor-moment system (weights sum 0, second moment 2, moments
+    4, 6, 8 vanish) solved with ``numpy.linalg.solve`` as the reference does,
+    so the coefficient bits are the reference's on the same host."""
+    moments = [0, 2, 4, 6, 8]
+    a = np.zeros((5, 5))
+    rhs = np.zeros(5)
+    for r, m in enumerate(moments):
+        a[r, 0] = 1.0 if m == 0 else 0.0
+        for n in range(1, 5):
+            a[r, n] = 2.0 * n ** m
+        if m == 2:
+            rhs[r] = 2.0
+    return StencilCoeffs8(*np.linalg.solve(a, rhs))
+
+
+def wide4_amplification(diffusivity: float, dt: float, geom: Geometry, modes=(1, 1, 1),
+                        coeffs: StencilCoeffs8 | None = None) -> float:
+    """Per-step amplification of a cosine mode under the 9-point operator."""
+    c = (coeffs if coeffs is not None else derive_coeffs8()).as_array()
+    n = geom.domain.extents
+    g = 1.0
+    for d in range(3):
+        theta = 2.0 * math.pi * modes[d] / n[d]
+        s = c[0] + 2.0 * sum(c[k] * math.cos(k * theta) for k in range(1, 5))
+        g += diffusivity * dt * s / geom.dx[d] ** 2
+    return g
+
+
+def wide4_stable_dt(diffusivity: float, dx, safety: float = 0.9) -> float:
+    """dt at ``safety`` times the forward-Euler bound of the 9-point operator."""
+    if isinstance(dx, (int, float)):
+        dx = (float(dx),) * 3
+    c = derive_coeffs8().as_array()
+    s_pi = abs(c[0] + 2.0 * sum(c[k] * math.cos(k * math.pi) for k in range(1, 5)))
+    lam = diffusivity * s_pi * sum(1.0 / d ** 2 for d in dx)
+    return safety * 2.0 / lam
+
+
+def wide4_plan(mf: MultiFab, max_rows: int | None = None, nctas: int | None = None) -> "_native.MarchPlan":
+    """Columns (full box width, <= 16 rows (8 when wider than 64), full z)
+    split into equal plane shares over one persistent CTA per SM."""
+    from .march import march_columns, sm_count
+
+    widest = max((mf.units[u].valid.extents[0] for u in mf.local_units), default=1)
+    if widest > 128:
+        raise ValueError("wide4 kernel supports boxes up to 128 cells wide in x")
+    rows = max_rows or (16 if widest <= 64 else 8)
+    key = ("wide4", rows, nctas, mf.layout, tuple(mf.local_units))
+    plan = mf._plans.get(key)
+    if plan is None:
+        cols = march_columns(mf, rows, packed=False)
+        plan = _native.MarchPlan(cols, nctas or sm_count(mf.device))
+        mf._plans[key] = plan
+    return plan
+
+
+def _check(mf_new: MultiFab, mf_old: MultiFab) -> None:
+    if mf_new.ncomp != 1 or mf_old.ncomp != 1:
+        raise ValueError("stencil kernels operate on single-component MultiFabs")
+    if mf_old.nghost < RADIUS:
+        raise ValueError("wide4 kernel requires nghost >= 4")
+    if not mf_new.same_layout(mf_old):
+        raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
+    if mf_new.data.data_ptr() == mf_old.data.data_ptr():
+        raise ValueError("wide4_step needs distinct old/new MultiFabs (double buffering)")
+
+
+def _launch(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: float, dt: float,
+            coeffs: StencilCoeffs8 | None, max_rows: int | None = None, nctas: int | None = None) -> None:
+    c = coeffs if coeffs is not None else derive_coeffs8()
+    dxi2 = tuple(1.0 / d ** 2 for d in geom.dx)
+    dtD = diffusivity * dt
+    plan = wide4_plan(mf_old, max_rows, nctas)
+    if plan.ncolumns == 0:
+        return
+    cbuf = (ctypes.c_double * 5)(c.c0, c.c1, c.c2, c.c3, c.c4)
+    _native.check(_native.load().tm_wide4_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr, 1,
+                                                ctypes.cast(cbuf, ctypes.c_void_p), dxi2[0], dxi2[1], dxi2[2],
+                                                dtD, mf_old.stream()), "tm_wide4_march")
+
+
+def wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: float, dt: float,
+               schedule=None, workers: int = 1, coeffs: StencilCoeffs8 | None = None) -> None:
+    """u_new = u_old + dt*D*(8th-order Laplacian) on every valid cell; the 4
+    ghost layers of ``mf_old`` must be filled beforehand.  ``schedule`` and
+    ``workers`` are accepted for API parity (the result does not depend on
+    the tiling, reference test_kernels.py:360-368): the device
+    decomposition is the persistent column march."""
+    _check(mf_new, mf_old)
+    _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)
+
+
+def loop_wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: float, dt: float,
+                    workers: int = 1, coeffs: StencilCoeffs8 | None = None) -> None:
+    """The reference's loop-level baseline (z loop split over threads) is a
+    CPU threading variant of the same arithmetic; on the device it is the
+    same kernel."""
+    _check(mf_new, mf_old)
+    _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)

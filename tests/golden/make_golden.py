@@ -19,6 +19,10 @@ host-independent).  Outputs:
 * fills.npz  -- reference FillBoundary results (sentinel + linear field)
 * heat.npz   -- sha256 of initial/final global arrays, reduce_sum values,
                 and full final arrays for the small cases
+* wide4.npz  -- reference wide4_step runs (nghost 4): the coefficient and dt
+                bits used, per-step reduce_sum, sha256 / full final arrays
+
+``python tests/golden/make_golden.py wide4`` regenerates only wide4.npz.
 """
 
 from __future__ import annotations
@@ -208,7 +212,60 @@ def make_heat():
     np.savez_compressed(os.path.join(HERE, "heat.npz"), **out)
 
 
+WIDE4_CASES = [  # (name, n, max_grid_size, steps, keep full field)
+    ("w16_single", 16, 16, 3, True),
+    ("w32_boxes", 32, 16, 3, True),
+    ("w32_small_boxes", 32, 8, 2, False),
+    ("w30_uneven", 30, 13, 2, True),
+    ("w64_c2like", 64, 32, 2, False),
+]
+
+
+def make_wide4():
+    """Reference wide4 runs (kernels.wide4_step, SURVEY.md §8f row 1): fill;
+    step; swap, nghost 4, fully periodic, seeded gauss+noise init."""
+    import dataclasses
+
+    from tilemesh.kernels import derive_coeffs8, wide4_stable_dt, wide4_step
+
+    out = {}
+    coeffs = derive_coeffs8()
+    out["coeffs"] = coeffs.as_array()
+    for name, n, mgs, steps, keep_full in WIDE4_CASES:
+        w = dataclasses.replace(CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
+        glob = make_init(w)
+        dom = w.domain
+        geom = Geometry(dom, (True, True, True), (w.dx,) * 3)
+        old = MultiFab(BoxArray.chop(dom, w.max_grid_size), 1, 4)
+        set_global(old, glob)
+        new = old.clone_empty()
+        plan = build_fill_plan(old, geom)
+        sched = build_schedule(old, w.tile_size)
+        dt = wide4_stable_dt(1.0, geom.dx)
+        sums = []
+        for _ in range(steps):
+            fill_boundary(old, geom, plan)
+            wide4_step(new, old, geom, 1.0, dt, sched, 1, coeffs)
+            old, new = new, old
+            sums.append(old.reduce_sum(0))
+        fin = get_global(old, n)
+        out[name + "/init_sha"] = np.array(sha(glob))
+        out[name + "/final_sha"] = np.array(sha(fin))
+        out[name + "/sums"] = np.array(sums)
+        out[name + "/dt"] = np.array(dt)
+        out[name + "/meta"] = np.array(json.dumps(dict(n=n, mgs=mgs, steps=steps)))
+        if keep_full:
+            out[name + "/final"] = fin
+        print(f"wide4 {name}: sum {sums[-1]} sha {sha(fin)[:16]}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "wide4.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference:", tilemesh.__file__)
-    make_plans_and_fills()
-    make_heat()
+    which = sys.argv[1:] or ["plans", "heat", "wide4"]
+    if "plans" in which:
+        make_plans_and_fills()
+    if "heat" in which:
+        make_heat()
+    if "wide4" in which:
+        make_wide4()

@@ -1,0 +1,184 @@
+"""wide4 (9-point 8th-order Laplacian, nghost 4) on the
+B200: bit-identical to the reference's own runs (tests/golden/wide4.npz,
+made by tests/golden/make_golden.py from /root/reference) and to the oracle
+on other layouts; plus the reference's own property tests
+(test_kernels.py:330-427, test_acceptance.py:193-216)."""
+
+import dataclasses
+import hashlib
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.fixture(scope="module")
+def tm():
+    import torch
+
+    import paper_1604_03570_b200 as tm
+
+    torch.cuda.set_device(0)
+    return tm
+
+
+def run_device(tm, w, glob, coeffs, dt, steps, max_rows=None, nctas=None):
+    from paper_1604_03570_b200.wide4 import _launch
+
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    old = tm.MultiFab(ba, 1, 4)
+    old.from_global(glob)
+    new = old.clone_empty()
+    plan = tm.build_fill_plan(old, geom)
+    sums = []
+    for _ in range(steps):
+        tm.fill_boundary(old, geom, plan)
+        if max_rows is None and nctas is None:
+            tm.wide4_step(new, old, geom, 1.0, dt, None, 1, coeffs)
+        else:
+            _launch(new, old, geom, 1.0, dt, coeffs, max_rows, nctas)
+        old, new = new, old
+        sums.append(old.reduce_sum())
+    return old, sums
+
+
+def test_wide4_matches_reference_runs(tm):
+    z = np.load(os.path.join(G, "wide4.npz"))
+    coeffs = tm.StencilCoeffs8(*[float(v) for v in z["coeffs"]])
+    names = sorted({k.split("/")[0] for k in z.files if "/" in k})
+    for name in names:
+        m = json.loads(str(z[name + "/meta"]))
+        w = dataclasses.replace(tm.CONFIGS["C1"].scaled(m["n"], m["mgs"], m["steps"]), nghost=4)
+        glob = tm.make_init(w)
+        mf, sums = run_device(tm, w, glob, coeffs, float(z[name + "/dt"]), w.steps)
+        fin = mf.to_global().cpu().numpy()
+        assert sha(fin) == str(z[name + "/final_sha"]), name
+        assert sums == list(z[name + "/sums"]), name
+
+
+@pytest.mark.parametrize("n,mgs,steps,rows,nctas", [
+    (40, 40, 2, None, None),   # 40-wide boxes: 2 cells per lane, partial lanes
+    (37, 37, 2, None, 5),      # odd width, odd height
+    (128, 128, 1, None, None),  # 128-wide: 4 cells per lane, 8-row columns
+    (96, 48, 2, 5, 7),         # 5-row columns, segments crossing columns
+    (24, 4, 2, None, None),    # 4^3 boxes: every ghost layer from a neighbour box
+])
+def test_wide4_matches_oracle(tm, n, mgs, steps, rows, nctas):
+    w = dataclasses.replace(tm.CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
+    glob = tm.make_init(w)
+    coeffs = tm.derive_coeffs8()
+    dt = tm.wide4_stable_dt(1.0, (w.dx,) * 3)
+    mf, _ = run_device(tm, w, glob, coeffs, dt, steps, rows, nctas)
+    want = orc.wide4_periodic(glob[0], steps, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
+    assert np.array_equal(mf.to_global().cpu().numpy()[0], want)
+
+
+def test_wide4_constant_unchanged(tm):
+    dom = tm.Box((0, 0, 0), (15, 15, 15))
+    geom = tm.Geometry(dom, (True, True, True), (1.0 / 16,) * 3)
+    mf = tm.MultiFab(tm.BoxArray([dom]), 1, 4)
+    mf.fill(4.5)
+    out = mf.clone_empty()
+    dt = tm.wide4_stable_dt(1.0, geom.dx[0])
+    for _ in range(3):
+        tm.fill_boundary(mf, geom)
+        tm.wide4_step(out, mf, geom, 1.0, dt, None)
+        mf, out = out, mf
+    assert np.all(mf.grid_valid_array(0) == 4.5)
+
+
+def test_wide4_quadratic_laplacian_exact(tm):
+    """u = i^2 + j^2 + k^2 (ghosts set analytically, no fill) has discrete
+    Laplacian exactly 6 with dx = 1."""
+    import torch
+
+    dom = tm.Box((0, 0, 0), (11, 11, 11))
+    geom = tm.Geometry(dom, (True, True, True), (1.0, 1.0, 1.0))
+    mf = tm.MultiFab(tm.BoxArray([dom]), 1, 4)
+    f = mf.fab(0)
+    b = f.abox
+    I, J, K = np.ogrid[b.lo[0]:b.hi[0] + 1, b.lo[1]:b.hi[1] + 1, b.lo[2]:b.hi[2] + 1]
+    f.view(b, 0, 1)[..., 0].copy_(torch.from_numpy(np.ascontiguousarray((I ** 2 + J ** 2 + K ** 2).astype(float))))
+    out = mf.clone_empty()
+    dt, D = 1e-3, 2.0
+    tm.wide4_step(out, mf, geom, D, dt, None)
+    want = mf.grid_valid_array(0) + dt * D * 6.0
+    assert np.max(np.abs(out.grid_valid_array(0) - want)) <= 1e-11
+
+
+def test_wide4_symbol_amplification(tm):
+    dom = tm.Box((0, 0, 0), (15, 15, 15))
+    geom = tm.Geometry(dom, (True, True, True), (1.0 / 16,) * 3)
+    mf = tm.MultiFab(tm.BoxArray([dom]), 1, 4)
+    tm.init_cosine(mf, geom, modes=(1, 2, 3))
+    u0 = mf.grid_valid_array(0).copy()
+    dt = tm.wide4_stable_dt(1.0, geom.dx[0])
+    out = mf.clone_empty()
+    for _ in range(4):
+        tm.fill_boundary(mf, geom)
+        tm.wide4_step(out, mf, geom, 1.0, dt, None)
+        mf, out = out, mf
+    g4 = tm.wide4_amplification(1.0, dt, geom, modes=(1, 2, 3)) ** 4
+    rel = np.max(np.abs(mf.grid_valid_array(0) - g4 * u0)) / np.max(np.abs(g4 * u0))
+    assert rel <= 1e-12
+
+
+def test_wide4_order_at_least_7_5(tm):
+    def err(n):
+        dom = tm.Box((0, 0, 0), (n - 1, n - 1, n - 1))
+        geom = tm.Geometry(dom, (True, True, True), (1.0 / n,) * 3)
+        mf = tm.MultiFab(tm.BoxArray([dom]), 1, 4)
+        tm.init_cosine(mf, geom)
+        out = mf.clone_empty()
+        tm.fill_boundary(mf, geom)
+        tm.wide4_step(out, mf, geom, 1.0, 1.0, None)
+        lap_h = out.grid_valid_array(0) - mf.grid_valid_array(0)
+        lap = -3.0 * (2.0 * math.pi) ** 2 * mf.grid_valid_array(0)
+        return float(np.max(np.abs(lap_h - lap)))
+
+    assert math.log2(err(16) / err(32)) >= 7.5
+
+
+def test_wide4_tiling_and_loop_variant_bitwise(tm):
+    w = dataclasses.replace(tm.CONFIGS["C1"].scaled(32, 16, 2), nghost=4)
+    glob = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    dt = tm.wide4_stable_dt(1.0, geom.dx)
+    outs = []
+    for variant in ("tiled", "loop"):
+        mf = tm.MultiFab(tm.BoxArray.chop(w.domain, 16), 1, 4)
+        mf.from_global(glob)
+        out = mf.clone_empty()
+        for _ in range(2):
+            tm.fill_boundary(mf, geom)
+            if variant == "tiled":
+                tm.wide4_step(out, mf, geom, 1.0, dt, tm.build_schedule(mf, (8, 4, 4)), workers=3)
+            else:
+                tm.loop_wide4_step(out, mf, geom, 1.0, dt, workers=2)
+            mf, out = out, mf
+        outs.append(mf.to_global().cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
+
+
+def test_wide4_needs_four_ghosts(tm):
+    dom = tm.Box((0, 0, 0), (7, 7, 7))
+    geom = tm.Geometry(dom, (True, True, True), (1.0 / 8,) * 3)
+    mf = tm.MultiFab(tm.BoxArray([dom]), 1, 1)
+    with pytest.raises(ValueError):
+        tm.wide4_step(mf.clone_empty(), mf, geom, 1.0, 1e-5, None)
+    mf2 = tm.MultiFab(tm.BoxArray([dom]), 2, 4)
+    with pytest.raises(ValueError):
+        tm.wide4_step(mf2.clone_empty(), mf2, geom, 1.0, 1e-5, None)
