@@ -314,7 +314,7 @@ def run_ours(args, w):
     runner.reset()  # state was advanced outside the runner's bookkeeping
     peak, peak_src = peaks()
     achieved = BYTES_PER_CELL * local_cells / (kern_ms * 1e-3) / 1e9
-    ghost_cells = sum(t.dst_box.ncells for t in plan.tags if mf.dm[t.dst_unit] == mf.rank) * w.ncomp
+    ghost_cells = sum(t.dst_box.ncells for t in plan.tags if mf.unit_owner[t.dst_unit] == mf.rank) * w.ncomp
     fill_gbs = 16 * ghost_cells / (fill_ms * 1e-3) / 1e9
 
     # --- end-to-end through the public API with host buffers -------------

@@ -448,7 +448,7 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
     bool even2 = true, even4 = true;
     for (int64_t b = 0; b < nblocks; ++b) {
         const tm_block &k = blocks[b];
-        if (k.nx < 1 || k.ny < 1 || k.nz < 1 || k.slot < 0 || k.x0 < 1 || k.y0 < 1 || k.z0 < 1)
+        if (k.nx < 1 || k.ny < 1 || k.nz < 1 || k.slot < 0 || k.x0 < 0 || k.y0 < 0 || k.z0 < 0)
             return fail(TM_ERR_INVALID, "tm_sweep_plan_create: malformed block " + std::to_string(b));
         mx = std::max(mx, k.nx);
         my = std::max(my, k.ny);

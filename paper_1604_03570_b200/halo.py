@@ -75,7 +75,7 @@ class HaloExchange:
 
         self.device = mf.device
         tags = plan.tags
-        _, sends, recvs = exchange_lists(mf.dm.owners, tags, mf.rank)
+        _, sends, recvs = exchange_lists(mf.unit_owner, tags, mf.rank)
         nc = mf.ncomp
 
         def build(groups, remote_side_is_dst):

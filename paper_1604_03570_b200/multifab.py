@@ -24,7 +24,7 @@ from typing import Callable, NamedTuple
 import numpy as np
 
 from . import _native
-from .box import Box, decompose, grow, split_extent
+from .box import Box, check_tile_size, decompose, grow, split_extent
 from .boxarray import BoxArray, DistributionMapping, Geometry
 from .fillplan import FillPlan, build_fill_plan
 from .mfiter import TileSchedule, build_schedule
@@ -97,6 +97,18 @@ class StorageLayout(NamedTuple):
 
     def to_c(self) -> "_native.tm_layout":
         return _native.tm_layout(*self)
+
+
+def unit_boxes(ba, layout: str = CONTIGUOUS, region_size=None):
+    """(unit valid boxes, owning grid per unit): one unit per grid
+    (contiguous) or the grid's regions, ``decompose(grid, region_size)`` in
+    grid order (regional, level.py:124-133).  Host-only."""
+    valids, grid_of = [], []
+    for g, grid in enumerate(ba):
+        for v in ([grid] if layout == CONTIGUOUS else decompose(grid, check_tile_size(region_size))):
+            valids.append(v)
+            grid_of.append(g)
+    return valids, grid_of
 
 
 class Unit(NamedTuple):
@@ -186,7 +198,7 @@ class MultiFab:
         if layout == REGIONAL:
             if region_size is None:
                 raise ValueError("regional layout requires a region_size")
-            raise NotImplementedError("regional layout is not on the device path yet (DESIGN.md §7)")
+            region_size = check_tile_size(region_size)
         if not torch.cuda.is_available():
             raise _native.TilemeshError("tilemesh_b200 MultiFab needs a CUDA device (no CPU fallback)")
         self.ba = ba
@@ -200,8 +212,9 @@ class MultiFab:
         self.dm = dm
         self.rank = crank if rank is None else rank
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
-        valids = list(ba)
-        self.local_units = [u for u in range(len(valids)) if dm[u] == self.rank]
+        valids, grid_of = unit_boxes(ba, layout, region_size)
+        self.unit_owner = tuple(dm[g] for g in grid_of)  # a unit lives with its grid
+        self.local_units = [u for u in range(len(valids)) if self.unit_owner[u] == self.rank]
         self.slot_of = {u: s for s, u in enumerate(self.local_units)}
         self.layout = StorageLayout.for_units([valids[u] for u in self.local_units], ncomp, nghost)
         L = self.layout
@@ -213,7 +226,7 @@ class MultiFab:
             fab = None
             if u in self.slot_of:
                 fab = DeviceFab(self, self.slot_of[u], grow(v, nghost) if nghost > 0 else v)
-            self.units.append(Unit(u, v, fab))
+            self.units.append(Unit(grid_of[u], v, fab))
         self._plans: dict = {}
         self._unit_sweep = None
         self._scratch = {}
@@ -227,7 +240,7 @@ class MultiFab:
     def fab(self, u: int) -> DeviceFab:
         f = self.units[u].fab
         if f is None:
-            raise KeyError(f"unit {u} is owned by rank {self.dm[u]}, not {self.rank}")
+            raise KeyError(f"unit {u} is owned by rank {self.unit_owner[u]}, not {self.rank}")
         return f
 
     def __getitem__(self, mfi) -> DeviceFab:
@@ -318,8 +331,41 @@ class MultiFab:
 
     def grid_valid_array(self, g: int, comp: int = 0) -> np.ndarray:
         """Valid data of grid ``g`` as a host ``(nx, ny, nz)`` array (level.py:152-167)."""
-        u = self.units[g]
-        return np.asfortranarray(self.fab(g).view(u.valid, comp, 1)[..., 0].cpu().numpy())
+        if self.layout_kind == CONTIGUOUS:
+            u = self.units[g]
+            return np.asfortranarray(self.fab(g).view(u.valid, comp, 1)[..., 0].cpu().numpy())
+        grid = self.ba[g]
+        out = np.empty(grid.extents, order="F")
+        for u, unit in enumerate(self.units):
+            if unit.grid != g:
+                continue
+            sl = tuple(slice(unit.valid.lo[d] - grid.lo[d], unit.valid.hi[d] - grid.lo[d] + 1) for d in range(3))
+            out[sl] = self.fab(u).view(unit.valid, comp, 1)[..., 0].cpu().numpy()
+        return out
+
+    def _grid_shadow(self) -> "MultiFab":
+        """Regional layout: a contiguous, ghost-free copy of the valid data (one
+        slot per grid, same distribution), refreshed by one copy launch.  The
+        reference checksum runs in grid order over whole grids, across region
+        boundaries (level.py:183-190), which is the contiguous kernel's order."""
+        sh = self._plans.get("grid_shadow")
+        if sh is None:
+            shadow = MultiFab(self.ba, self.ncomp, 0, dm=self.dm, device=self.device, rank=self.rank, zero=False)
+            L, S = self.layout, shadow.layout
+            tags = np.zeros(len(self.local_units), dtype=_native.COPY_TAG_DTYPE)
+            for t, u in enumerate(self.local_units):
+                unit = self.units[u]
+                v, gb = unit.valid, self.ba[unit.grid]
+                e = v.extents
+                dst = (shadow.slot_of[unit.grid] * S.slot + (v.lo[2] - gb.lo[2]) * S.plane
+                       + (v.lo[1] - gb.lo[1]) * S.row + S.xoff + (v.lo[0] - gb.lo[0]))
+                src = self.slot_of[u] * L.slot + L.nghost * L.plane + L.nghost * L.row + L.xoff
+                tags[t] = (dst, src, e[0], e[1], e[2], 0)
+            sh = (shadow, _native.CopyPlan(tags, self.ncomp))
+            self._plans["grid_shadow"] = sh
+        shadow, plan = sh
+        plan.run(shadow.ptr, shadow.layout.side(), self.ptr, self.layout.side(), self.stream())
+        return shadow
 
     # -------------------------------------------------------------- reductions
     def _check_reduce(self, comp: int) -> None:
@@ -355,6 +401,8 @@ class MultiFab:
         import torch
 
         self._check_reduce(comp)
+        if self.layout_kind == REGIONAL:
+            return self._grid_shadow().reduce_sum_device(comp)
         rank, world = comm_info()
         nunits = len(self.units)
         L = _native.load()
@@ -488,7 +536,7 @@ def _device_fill(mf: MultiFab, plan: FillPlan):
     if dev is None:
         from .halo import HaloExchange
 
-        owners = mf.dm.owners
+        owners = mf.unit_owner
         local = [t for t in plan.tags if owners[t.dst_unit] == mf.rank and owners[t.src_unit] == mf.rank]
         copy = _native.CopyPlan(local_copy_tags(mf, local), mf.ncomp)
         halo = HaloExchange(mf, plan) if mf.dm.nranks > 1 else None

@@ -22,7 +22,9 @@ host-independent).  Outputs:
 * wide4.npz  -- reference wide4_step runs (nghost 4): the coefficient and dt
                 bits used, per-step reduce_sum, sha256 / full final arrays
 
-``python tests/golden/make_golden.py wide4`` regenerates only wide4.npz.
+* regional.npz -- REGIONAL-layout units, plans, a fill, heat / wide4 runs
+
+``python tests/golden/make_golden.py wide4`` (or ``regional``, ...) regenerates one file.
 """
 
 from __future__ import annotations
@@ -260,12 +262,71 @@ def make_wide4():
     np.savez_compressed(os.path.join(HERE, "wide4.npz"), **out)
 
 
+REGIONAL_CASES = [  # (name, domain hi, max_grid_size or None, region, nghost, periodic, kernel, steps)
+    ("r24_one_grid", (23, 23, 23), None, (12, 12, 12), 1, (True, True, True), "heat", 5),
+    ("r32_uneven", (31, 31, 31), 16, (8, 16, 5), 2, (True, True, True), "heat", 3),
+    ("r_two_grids", (15, 7, 7), 8, (4, 4, 4), 2, (True, False, True), "fill", 0),
+    ("r32_wide4", (31, 31, 31), None, (16, 16, 16), 4, (True, True, True), "wide4", 2),
+]
+
+
+def make_regional():
+    """Reference runs on the REGIONAL layout (level.py:116-133; SURVEY.md §8f
+    row 3): the unit list, the FillBoundary plan over regions, a fill of a
+    linear field, and heat / wide4 runs with their reduce_sum values."""
+    from tilemesh.kernels import derive_coeffs8, wide4_stable_dt, wide4_step
+    from tilemesh.level import REGIONAL
+
+    out = {}
+    for name, hi, mgs, region, ng, per, kernel, steps in REGIONAL_CASES:
+        dom = Box((0, 0, 0), hi)
+        n = hi[0] + 1
+        geom = Geometry(dom, per, (1.0 / n,) * 3)
+        ba = BoxArray.chop(dom, (mgs,) * 3) if mgs else BoxArray([dom])
+        mf = MultiFab(ba, 1, ng, REGIONAL, region)
+        plan = build_fill_plan(mf, geom)
+        out[name + "/units"] = np.array([[u.grid, *u.valid.lo, *u.valid.hi] for u in mf.units], dtype=np.int64)
+        out[name + "/tags"] = tag_rows(plan.tags)
+        out[name + "/meta"] = np.array(json.dumps(dict(hi=hi, mgs=mgs, region=region, ng=ng, periodic=per,
+                                                       kernel=kernel, steps=steps)))
+        if kernel == "fill":
+            mf.fill(SENTINEL)
+            mf.set_from_function(f_linear)
+            fill_boundary(mf, geom, plan)
+            out[name + "/fill"] = np.concatenate([u.fab.flat for u in mf.units])
+            print(f"regional {name}: {len(mf.units)} units, {len(plan.tags)} tags", flush=True)
+            continue
+        w = CONFIGS["C1"].scaled(n, n, steps)
+        glob = make_init(w)
+        set_global(mf, glob)
+        new = mf.clone_empty()
+        sched = build_schedule(mf, (8, 8, 8))
+        sums = []
+        old = mf
+        for _ in range(steps):
+            fill_boundary(old, geom, plan)
+            if kernel == "heat":
+                heat_step(new, old, geom, HeatParams.stable(1.0, geom.dx), sched)
+            else:
+                wide4_step(new, old, geom, 1.0, wide4_stable_dt(1.0, geom.dx), sched, 1, derive_coeffs8())
+            old, new = new, old
+            sums.append(old.reduce_sum(0))
+        fin = get_global(old, n)
+        out[name + "/init_sha"] = np.array(sha(glob))
+        out[name + "/final_sha"] = np.array(sha(fin))
+        out[name + "/sums"] = np.array(sums)
+        print(f"regional {name}: {len(mf.units)} units, {len(plan.tags)} tags, sum {sums[-1]}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "regional.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference:", tilemesh.__file__)
-    which = sys.argv[1:] or ["plans", "heat", "wide4"]
+    which = sys.argv[1:] or ["plans", "heat", "wide4", "regional"]
     if "plans" in which:
         make_plans_and_fills()
     if "heat" in which:
         make_heat()
     if "wide4" in which:
         make_wide4()
+    if "regional" in which:
+        make_regional()
