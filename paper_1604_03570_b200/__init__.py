@@ -13,6 +13,7 @@ libtilemesh_b200.so (no CPU fallback).
 from .box import Box, box_diff, decompose, grow, intersect, shift, to_face
 from .boxarray import BoxArray, DistributionMapping, Geometry, partition
 from .configs import CONFIGS, Workload, make_init
+from .fab import FArrayBox, copy_region, intersect_copy
 from .fillplan import CopyTag, FillPlan, build_fill_plan, shift_candidates, split_tags
 from .mfiter import (
     DEFAULT_TILE_SIZE,
@@ -23,6 +24,7 @@ from .mfiter import (
     parallel_for_tiles,
 )
 from .multifab import CONTIGUOUS, REGIONAL, DeviceFab, FillBoundary, MultiFab, fill_boundary
+from .plotfile import read_plotfile, write_plotfile
 from .stencil import (
     HeatParams,
     gsrb_color,
@@ -45,10 +47,11 @@ from .wide4 import (
 __all__ = [
     "Box", "box_diff", "decompose", "grow", "intersect", "shift", "to_face",
     "BoxArray", "DistributionMapping", "Geometry", "partition",
-    "CONFIGS", "Workload", "make_init",
+    "CONFIGS", "Workload", "make_init", "FArrayBox", "copy_region", "intersect_copy",
     "CopyTag", "FillPlan", "build_fill_plan", "shift_candidates", "split_tags",
     "DEFAULT_TILE_SIZE", "MFIter", "TileCursor", "TileSchedule", "build_schedule", "parallel_for_tiles",
     "CONTIGUOUS", "REGIONAL", "DeviceFab", "FillBoundary", "MultiFab", "fill_boundary",
+    "read_plotfile", "write_plotfile",
     "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
     "residual_maxnorm",
     "StencilCoeffs8", "derive_coeffs8", "loop_wide4_step", "wide4_amplification", "wide4_stable_dt", "wide4_step",

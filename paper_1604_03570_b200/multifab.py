@@ -175,6 +175,18 @@ class DeviceFab:
         """Host copy in the reference layout: (nx, ny, nz, ncomp), F-order."""
         return np.asfortranarray(self.data.cpu().numpy())
 
+    @property
+    def flat(self) -> np.ndarray:
+        """Host copy of the reference's flat storage (x fastest, component slowest)."""
+        return self.to_numpy().ravel(order="F")
+
+    def offset(self, i: int, j: int, k: int, c: int = 0) -> int:
+        """Index of (i, j, k, c) in ``flat`` (reference fab.py:38-44)."""
+        self._check(i, j, k, c)
+        lo = self.abox.lo
+        nx, ny, nz = self.abox.extents
+        return (i - lo[0]) + nx * ((j - lo[1]) + ny * ((k - lo[2]) + nz * c))
+
 
 class MultiFab:
     """Device MultiFab with the reference constructor signature.

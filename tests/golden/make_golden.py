@@ -23,6 +23,7 @@ host-independent).  Outputs:
                 bits used, per-step reduce_sum, sha256 / full final arrays
 
 * regional.npz -- REGIONAL-layout units, plans, a fill, heat / wide4 runs
+* plotfile.npz -- reference write_plotfile output (HEADER + unit fab bytes)
 
 ``python tests/golden/make_golden.py wide4`` (or ``regional``, ...) regenerates one file.
 """
@@ -319,9 +320,44 @@ def make_regional():
     np.savez_compressed(os.path.join(HERE, "regional.npz"), **out)
 
 
+def make_plotfiles():
+    """Reference plotfile-lite dumps (level.py:326-345, fab.py:86-90): the
+    HEADER text and every unit file's bytes."""
+    import tempfile
+
+    from tilemesh.level import REGIONAL, write_plotfile
+
+    out = {}
+    cases = [
+        ("p_two_comp", Box((0, 0, 0), (5, 5, 5)), None, 2, 1, None, False),
+        ("p_chop_ng2", Box((0, 0, 0), (11, 11, 11)), 6, 1, 2, None, True),
+        ("p_regional", Box((0, 0, 0), (15, 15, 15)), None, 1, 1, (8, 8, 16), True),
+    ]
+    for name, dom, mgs, nc, ng, region, fill in cases:
+        n = dom.hi[0] + 1
+        geom = Geometry(dom, (True, True, True), (1.0 / n,) * 3)
+        ba = BoxArray.chop(dom, (mgs,) * 3) if mgs else BoxArray([dom])
+        mf = MultiFab(ba, nc, ng, REGIONAL if region else "contiguous", region)
+        for c in range(nc):
+            mf.set_from_function(lambda i, j, k, c=c: f_linear(i, j, k) + 1000.0 * c + 0.125, comp=c)
+        if fill:
+            fill_boundary(mf, geom)
+        with tempfile.TemporaryDirectory() as d:
+            write_plotfile(mf, geom, d)
+            out[name + "/HEADER"] = np.array(open(os.path.join(d, "HEADER")).read())
+            files = sorted(f for f in os.listdir(d) if f.endswith(".fab"))
+            out[name + "/files"] = np.array(files)
+            for f in files:
+                out[name + "/" + f] = np.frombuffer(open(os.path.join(d, f), "rb").read(), dtype=np.uint8)
+        out[name + "/meta"] = np.array(json.dumps(dict(hi=dom.hi, mgs=mgs, nc=nc, ng=ng, region=region,
+                                                       fill=fill)))
+        print(f"plotfile {name}: {len(files)} unit files", flush=True)
+    np.savez_compressed(os.path.join(HERE, "plotfile.npz"), **out)
+
+
 if __name__ == "__main__":
     print("reference:", tilemesh.__file__)
-    which = sys.argv[1:] or ["plans", "heat", "wide4", "regional"]
+    which = sys.argv[1:] or ["plans", "heat", "wide4", "regional", "plotfile"]
     if "plans" in which:
         make_plans_and_fills()
     if "heat" in which:
@@ -330,3 +366,5 @@ if __name__ == "__main__":
         make_wide4()
     if "regional" in which:
         make_regional()
+    if "plotfile" in which:
+        make_plotfiles()
