@@ -5,16 +5,13 @@
 // gathers domain-shaped arrays: only the addressing of each side (tm_side)
 // changes.
 //
-// Work decomposition: all tags' elements (cells x components, x fastest) form
-// one flattened stream with a prefix-sum offset per tag.  CTA b owns stream
-// elements [b*kItemElems, (b+1)*kItemElems); each thread takes kBatch
-// elements strided by the CTA width, locates their tags by binary search in a
-// shared-memory copy of the CTA's slice of the prefix array, and issues all
-// kBatch loads before any store.  Corner tags of one cell and face tags of
-// thousands of cells therefore cost the same per element, and every load of
-// a CTA is in flight at once.  Consecutive threads take consecutive x cells,
-// so y/z-face rows are coalesced; x-face tags (ex = nghost) are strided by
-// the row pitch by nature of the layout.
+// Work decomposition: a tag is ey*ez*ncomp rows of ex contiguous cells.  The
+// plan cuts every tag into warp tasks of whole rows -- 32 rows per task when
+// rows are short (ex <= 16: x-face ghost columns, one row per lane), about
+// 512 cells per task when they are long (y/z faces, gathers; lanes across x)
+// -- so a row's address is computed once, not per element, and x-face rows,
+// which cost a DRAM chunk each whatever their width, are all in flight at
+// once.  Warps stride over the task list; the grid is one wave.
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -24,75 +21,126 @@
 namespace {
 
 constexpr int kCopyThreads = 256;
-constexpr int kBatch = 8;
-constexpr int64_t kItemElems = (int64_t)kCopyThreads * kBatch;
-constexpr int kMaxSpan = 128;  // tags staged in shared memory per CTA
+constexpr int kWarps = kCopyThreads / 32;
+constexpr uint32_t kShortRow = 8;        // rows up to this width: one row per lane
+constexpr int64_t kLongTaskCells = 256;  // target cells per task for long rows
 
-struct WorkItem {
-    int32_t t0, t1;  // tags holding the first / last element of the item
+// A run of nrows consecutive y rows of one (z, component) slice of a tag:
+// every row of a task starts one side-row stride after the previous.
+struct Task {
+    int64_t src_off, dst_off;  // the tag's
+    int32_t ex, ey, ez;        // the tag's
+    int32_t y0, z;
+    uint16_t c, nrows;
 };
 
 struct SideDev {
     int64_t sy, sz, sc;
 };
 
-__device__ __forceinline__ int64_t side_offset(const SideDev &s, uint32_t x, uint32_t y, uint32_t z, uint32_t c,
-                                               uint32_t ex, uint32_t ey, uint32_t ez) {
-    if (s.sy == 0) {  // packed per tag
-        return (int64_t)x + (int64_t)ex * ((int64_t)y + (int64_t)ey * ((int64_t)z + (int64_t)ez * c));
-    }
-    return (int64_t)x + s.sy * y + s.sz * z + s.sc * c;
+// offset of cell (0, y, z, c) of a tag on one side; sy == 0: packed per tag
+__device__ __forceinline__ int64_t cell_offset(const SideDev &s, int64_t y, int64_t z, int64_t c, int64_t ex,
+                                               int64_t ey, int64_t ez) {
+    if (s.sy == 0) return ex * (y + ey * (z + ez * c));
+    return s.sy * y + s.sz * z + s.sc * c;
 }
 
-__global__ void __launch_bounds__(kCopyThreads) copy_tags_kernel(double *__restrict__ dst, SideDev ds,
-                                                                 const double *__restrict__ src, SideDev ss,
-                                                                 uint32_t ncomp, const tm_copy_tag *__restrict__ tags,
-                                                                 const int64_t *__restrict__ prefix,
-                                                                 const WorkItem *__restrict__ items, int64_t total) {
-    __shared__ int64_t sp[kMaxSpan + 1];
-    __shared__ tm_copy_tag st[kMaxSpan];
-    const WorkItem w = items[blockIdx.x];
-    const int span = w.t1 - w.t0 + 1;
-    const bool staged = span <= kMaxSpan;
-    if (staged) {
-        for (int i = threadIdx.x; i <= span; i += kCopyThreads) sp[i] = prefix[w.t0 + i];
-        for (int i = threadIdx.x; i < span; i += kCopyThreads) st[i] = tags[w.t0 + i];
-    }
-    __syncthreads();
-    const int64_t e0 = (int64_t)blockIdx.x * kItemElems;
-    const int64_t e1 = min(e0 + kItemElems, total);
-    const int64_t *P = staged ? sp : prefix + w.t0;
-    const tm_copy_tag *T = staged ? st : tags + w.t0;
-
-    double v[kBatch];
-    int64_t doff[kBatch];
+__global__ void __launch_bounds__(kCopyThreads, 3) copy_tags_kernel(double *__restrict__ dst, SideDev ds,
+                                                                    const double *__restrict__ src, SideDev ss,
+                                                                    const Task *__restrict__ tasks, int64_t ntasks) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * kWarps;
+    int64_t k = (int64_t)blockIdx.x * kWarps + (threadIdx.x >> 5);
+    Task nxt;
+    if (k < ntasks) nxt = tasks[k];
+    for (; k < ntasks; k += nw) {
+        const Task tk = nxt;  // the next task's descriptor is in flight while this one copies
+        if (k + nw < ntasks) nxt = tasks[k + nw];
+        const int64_t ex = tk.ex, ey = tk.ey, ez = tk.ez;
+        const int64_t sy = ss.sy == 0 ? ex : ss.sy, dy = ds.sy == 0 ? ex : ds.sy;  // row strides
+        const double *s0 = src + tk.src_off + cell_offset(ss, tk.y0, tk.z, tk.c, ex, ey, ez);
+        double *d0 = dst + tk.dst_off + cell_offset(ds, tk.y0, tk.z, tk.c, ex, ey, ez);
+        if (ex <= kShortRow) {
+            // Short rows (x-face ghosts): lanes split a row (4 x 16 B, or 8 x 8 B when a
+            // row is odd-sized or unaligned) so one instruction touches 8 (4) rows, not 32;
+            // all of the task's loads are issued before its stores.
+            const bool vec = ((ex | ((uintptr_t)s0 >> 3) | ((uintptr_t)d0 >> 3) | sy | dy) & 1) == 0;
+            if (vec) {
+                const int sub = lane & 3, rr = lane >> 2;
+                double2 v[4];
 #pragma unroll
-    for (int u = 0; u < kBatch; ++u) {
-        const int64_t e = e0 + threadIdx.x + (int64_t)u * kCopyThreads;
-        doff[u] = -1;
-        if (e < e1) {
-            int lo = 0, hi = span - 1;  // largest i with P[i] <= e
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (P[mid] <= e) lo = mid;
-                else hi = mid - 1;
+                for (int i = 0; i < 4; ++i) {
+                    const int row = 8 * i + rr;
+                    if (row < tk.nrows && 2 * sub < ex)
+                        v[i] = __ldg(reinterpret_cast<const double2 *>(s0 + sy * row) + sub);
+                }
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int row = 8 * i + rr;
+                    if (row < tk.nrows && 2 * sub < ex) reinterpret_cast<double2 *>(d0 + dy * row)[sub] = v[i];
+                }
+            } else {
+                const int sub = lane & 7, rr = lane >> 3;
+                double v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = 4 * i + rr;
+                    if (row < tk.nrows && sub < ex) v[i] = __ldg(s0 + sy * row + sub);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = 4 * i + rr;
+                    if (row < tk.nrows && sub < ex) d0[dy * row + sub] = v[i];
+                }
             }
-            const tm_copy_tag g = T[lo];
-            const uint32_t local = (uint32_t)(e - P[lo]);
-            const uint32_t ex = g.ex, ey = g.ey, ez = g.ez;
-            const uint32_t x = local % ex;
-            const uint32_t r = local / ex;
-            const uint32_t y = r % ey;
-            const uint32_t r2 = r / ey;
-            const uint32_t z = r2 % ez;
-            const uint32_t c = r2 / ez;
-            v[u] = __ldg(src + g.src_off + side_offset(ss, x, y, z, c, ex, ey, ez));
-            doff[u] = g.dst_off + side_offset(ds, x, y, z, c, ex, ey, ez);
+        } else {
+            // Long rows (y/z faces, gathers): a task is <= 256 cells (or one row); lanes
+            // take 16-B pairs (8-B cells when odd-sized/unaligned) in row-major order, all
+            // loads of a pass before its stores.
+            const bool vec = ((ex | ((uintptr_t)s0 >> 3) | ((uintptr_t)d0 >> 3) | sy | dy) & 1) == 0;
+            const uint32_t w = vec ? (uint32_t)(ex / 2) : (uint32_t)ex;  // units per row
+            const uint32_t n = (uint32_t)tk.nrows * w;
+            for (uint32_t base = 0; base < n; base += 128) {
+                if (vec) {
+                    double2 v[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t q = base + lane + 32 * i;
+                        if (q < n) {
+                            const uint32_t r = q / w, x = q - r * w;
+                            v[i] = __ldg(reinterpret_cast<const double2 *>(s0 + sy * r) + x);
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t q = base + lane + 32 * i;
+                        if (q < n) {
+                            const uint32_t r = q / w, x = q - r * w;
+                            reinterpret_cast<double2 *>(d0 + dy * r)[x] = v[i];
+                        }
+                    }
+                } else {
+                    double v[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t q = base + lane + 32 * i;
+                        if (q < n) {
+                            const uint32_t r = q / w, x = q - r * w;
+                            v[i] = __ldg(s0 + sy * r + x);
+                        }
+                    }
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint32_t q = base + lane + 32 * i;
+                        if (q < n) {
+                            const uint32_t r = q / w, x = q - r * w;
+                            d0[dy * r + x] = v[i];
+                        }
+                    }
+                }
+            }
         }
     }
-#pragma unroll
-    for (int u = 0; u < kBatch; ++u)
-        if (doff[u] >= 0) dst[doff[u]] = v[u];
 }
 
 }  // namespace
@@ -100,11 +148,10 @@ __global__ void __launch_bounds__(kCopyThreads) copy_tags_kernel(double *__restr
 struct tm_copy_plan {
     int32_t ncomp = 1;
     int64_t ntags = 0;
-    int64_t nitems = 0;
+    int64_t ntasks = 0;
     int64_t elements = 0;
-    tm_copy_tag *d_tags = nullptr;
-    int64_t *d_prefix = nullptr;
-    WorkItem *d_items = nullptr;
+    Task *d_tasks = nullptr;
+    int grid = 0;
 };
 
 extern "C" {
@@ -116,44 +163,37 @@ int tm_copy_plan_create(const tm_copy_tag *tags, int64_t ntags, int32_t ncomp, t
     if (ntags < 0 || ncomp < 1 || (ntags > 0 && !tags))
         return fail(TM_ERR_INVALID, "tm_copy_plan_create: bad arguments");
     if (ntags >= (int64_t)INT32_MAX) return fail(TM_ERR_INVALID, "tm_copy_plan_create: too many tags");
-    std::vector<int64_t> prefix(ntags + 1, 0);
+    std::vector<Task> tasks;
+    int64_t total = 0;
     for (int64_t t = 0; t < ntags; ++t) {
         const tm_copy_tag &g = tags[t];
         if (g.ex < 1 || g.ey < 1 || g.ez < 1) return fail(TM_ERR_INVALID, "tm_copy_plan_create: empty tag");
-        const int64_t E = (int64_t)g.ex * g.ey * g.ez * ncomp;
-        if (E >= (int64_t)UINT32_MAX) return fail(TM_ERR_INVALID, "tm_copy_plan_create: tag too large");
-        prefix[t + 1] = prefix[t] + E;
-    }
-    const int64_t total = prefix[ntags];
-    const int64_t nitems = (total + kItemElems - 1) / kItemElems;
-    if (nitems > (int64_t)INT32_MAX) return fail(TM_ERR_INVALID, "tm_copy_plan_create: too many elements");
-    std::vector<WorkItem> items(nitems);
-    int64_t t = 0;
-    for (int64_t b = 0; b < nitems; ++b) {
-        const int64_t first = b * kItemElems, last = std::min(total, first + kItemElems) - 1;
-        while (prefix[t + 1] <= first) ++t;
-        int64_t t1 = t;
-        while (prefix[t1 + 1] <= last) ++t1;
-        items[b] = WorkItem{(int32_t)t, (int32_t)t1};
+        if (ncomp > 65535) return fail(TM_ERR_INVALID, "tm_copy_plan_create: too many components");
+        total += (int64_t)g.ex * g.ey * g.ez * ncomp;
+        const int64_t per = (uint32_t)g.ex <= kShortRow ? 32 : std::max<int64_t>(1, kLongTaskCells / g.ex);
+        for (int32_t c = 0; c < ncomp; ++c)
+            for (int32_t z = 0; z < g.ez; ++z)
+                for (int32_t y = 0; y < g.ey; y += (int32_t)per)
+                    tasks.push_back(Task{g.src_off, g.dst_off, g.ex, g.ey, g.ez, y, z, (uint16_t)c,
+                                         (uint16_t)std::min<int64_t>(per, g.ey - y)});
     }
     tm_copy_plan *p = new tm_copy_plan();
     p->ncomp = ncomp;
     p->ntags = ntags;
-    p->nitems = nitems;
+    p->ntasks = (int64_t)tasks.size();
     p->elements = total;
-    if (nitems > 0) {
-        cudaError_t e = cudaMalloc(&p->d_tags, sizeof(tm_copy_tag) * ntags);
-        if (e == cudaSuccess) e = cudaMalloc(&p->d_prefix, sizeof(int64_t) * (ntags + 1));
-        if (e == cudaSuccess) e = cudaMalloc(&p->d_items, sizeof(WorkItem) * nitems);
-        if (e == cudaSuccess) e = cudaMemcpy(p->d_tags, tags, sizeof(tm_copy_tag) * ntags, cudaMemcpyHostToDevice);
+    if (!tasks.empty()) {
+        int dev = 0, nsm = 148, per_sm = 8;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, copy_tags_kernel, kCopyThreads, 0);
+        const int64_t want = (p->ntasks + kWarps - 1) / kWarps;
+        p->grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * std::max(per_sm, 1)));
+        cudaError_t e = cudaMalloc(&p->d_tasks, sizeof(Task) * tasks.size());
         if (e == cudaSuccess)
-            e = cudaMemcpy(p->d_prefix, prefix.data(), sizeof(int64_t) * (ntags + 1), cudaMemcpyHostToDevice);
-        if (e == cudaSuccess)
-            e = cudaMemcpy(p->d_items, items.data(), sizeof(WorkItem) * nitems, cudaMemcpyHostToDevice);
+            e = cudaMemcpy(p->d_tasks, tasks.data(), sizeof(Task) * tasks.size(), cudaMemcpyHostToDevice);
         if (e != cudaSuccess) {
-            cudaFree(p->d_tags);
-            cudaFree(p->d_prefix);
-            cudaFree(p->d_items);
+            cudaFree(p->d_tasks);
             delete p;
             return cuda_fail(e, "tm_copy_plan_create");
         }
@@ -166,9 +206,7 @@ int tm_copy_plan_destroy(tm_copy_plan *plan) {
     if (!plan) return TM_OK;
     // tables may still be read by queued launches on any stream: drain before freeing
     cudaDeviceSynchronize();
-    cudaFree(plan->d_tags);
-    cudaFree(plan->d_prefix);
-    cudaFree(plan->d_items);
+    cudaFree(plan->d_tasks);
     delete plan;
     return TM_OK;
 }
@@ -179,12 +217,12 @@ int tm_copy_run(const tm_copy_plan *plan, double *dst, const tm_side *dst_side, 
                 const tm_side *src_side, void *stream) {
     using namespace tmk;
     if (!plan || !dst_side || !src_side) return fail(TM_ERR_INVALID, "tm_copy_run: null argument");
-    if (plan->nitems == 0) return TM_OK;
+    if (plan->ntasks == 0) return TM_OK;
     if (!dst || !src) return fail(TM_ERR_INVALID, "tm_copy_run: null buffer");
     SideDev ds{dst_side->sy, dst_side->sz, dst_side->sc};
     SideDev ss{src_side->sy, src_side->sz, src_side->sc};
-    copy_tags_kernel<<<(unsigned)plan->nitems, kCopyThreads, 0, as_stream(stream)>>>(
-        dst, ds, src, ss, (uint32_t)plan->ncomp, plan->d_tags, plan->d_prefix, plan->d_items, plan->elements);
+    copy_tags_kernel<<<(unsigned)plan->grid, kCopyThreads, 0, as_stream(stream)>>>(dst, ds, src, ss, plan->d_tasks,
+                                                                                   plan->ntasks);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tm_copy_run launch");
     return TM_OK;

@@ -622,11 +622,11 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const Marc
 template <bool PACKED, bool SCATTER>
 int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int cpl, int rows, int nctas,
                  int ncomp, size_t smem, cudaStream_t s) {
-    // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 8x4, 64 -> 16x4
+    // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
         if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
         if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<2, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
         return launch_march_one<2, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
     }
     if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp

@@ -32,6 +32,7 @@ from .mfiter import TileSchedule, build_schedule
 CONTIGUOUS = "contiguous"
 REGIONAL = "regional"
 ROW_ALIGN = 16  # doubles: 128 B
+GHOST_ROW_WIDTH = 8  # doubles: one 64-B DRAM chunk per x-ghost row segment
 
 # CTA tile limits of the sweep kernels (tm_stencil.cu): a block must fit the
 # TMA box (nx + 2 <= 256) and at most 64 warp-row segments of 32 cells.
@@ -72,8 +73,9 @@ class StorageLayout(NamedTuple):
             mz = max(v.extents[2] for v in valids)
         else:
             mx = my = mz = 1
-        xoff = _round_up(nghost, ROW_ALIGN)
-        pitch = _round_up(xoff + mx + nghost, ROW_ALIGN)
+        xoff = _round_up(max(nghost, GHOST_ROW_WIDTH), ROW_ALIGN)
+        # room for a full 64-B chunk on each side of the valid row (see local_copy_tags)
+        pitch = _round_up(xoff + mx + max(nghost, GHOST_ROW_WIDTH), ROW_ALIGN)
         return StorageLayout(len(valids), ncomp, nghost, pitch, my + 2 * nghost, mz + 2 * nghost, xoff)
 
     @property
@@ -535,6 +537,22 @@ def local_copy_tags(mf: MultiFab, tags) -> np.ndarray:
     out["dst_off"] = cell_offsets(mf, du, dlo)
     out["src_off"] = cell_offsets(mf, su, slo)
     out["ex"], out["ey"], out["ez"] = ext[:, 0], ext[:, 1], ext[:, 2]
+    # x-face ghost rows: a tag that fills ALL ghost columns on one x side of
+    # its rows copies a whole 64-B chunk instead of nghost isolated doubles:
+    # the chunk holds those ghosts plus row padding that nothing reads, so the
+    # write is a full DRAM chunk (no read-modify-write of a partial sector)
+    # and the source read costs the same chunk it touched anyway.  Other tags
+    # never write these rows' ghost columns (plan tags are disjoint in dst).
+    ng, W = mf.nghost, GHOST_ROW_WIDTH
+    if 0 < ng < W:
+        vlo = np.array([mf.units[u].valid.lo[0] for u in range(len(mf.units))], dtype=np.int64)
+        vhi = np.array([mf.units[u].valid.hi[0] for u in range(len(mf.units))], dtype=np.int64)
+        full = ext[:, 0] == ng
+        left = full & (dlo[:, 0] == vlo[du] - ng)
+        right = full & (dlo[:, 0] == vhi[du] + 1)
+        out["dst_off"][left] -= W - ng
+        out["src_off"][left] -= W - ng
+        out["ex"][left | right] = W
     return out
 
 
