@@ -141,10 +141,13 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  * side 1 = i = hi+1).  xh_new != NULL additionally scatters every box's
  * boundary values into its face neighbours' halos in unew / xh_new
  * (d_nbr: 6 neighbour slots per slot, order -x,+x,-y,+y,-z,+z, -1 = none):
- * the fused FillBoundary of the next step.  Face halos only (7-point). */
+ * the fused FillBoundary of the next step.  Face halos only (7-point).
+ * reverse != 0 (scatter mode only): every CTA walks its columns in reverse
+ * order and marches z downward -- same results; a step that follows a
+ * forward step then starts on the planes that step wrote last (L2-resident). */
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
-                  const double *xh_old, double *xh_new, const int32_t *d_nbr, void *stream);
+                  const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);
 
 /* Fused red (0) / black (1) Gauss-Seidel pass of the column march, in place on
  * phi (ncomp 1), x halos from the packed buffer xh, and the updated colour's

@@ -84,7 +84,7 @@ def load():
     L.tm_reduce_minmax.argtypes = [vp, P(tm_layout), vp, i32, vp, vp]
     L.tm_march_plan_create.argtypes = [vp, i64, i32, P(vp)]
     L.tm_march_plan_destroy.argtypes = [vp]
-    L.tm_heat_march.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, vp]
+    L.tm_heat_march.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, i32, vp]
     L.tm_gsrb_march.argtypes = [vp, P(tm_layout), vp, P(tm_layout), vp, i32, f64, vp, vp, vp]
     L.tm_wide4_march.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp]
     for name in EXPORTS:

@@ -77,7 +77,7 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
 // bytes); empty[s] completes when all NWARP consumer warps released it.  No
 // CTA-wide barrier in the steady state: fast warps run ahead up to the ring
 // depth while the producer refills each stage as soon as it is free.
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV>
 __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const __grid_constant__ CUtensorMap xmap,
                                                                  MarchArgs a) {
@@ -110,15 +110,15 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     if (warp == NWARP) {  // ---------------- producer warp ----------------
         if (lane == 0) {
             int p = 0;
-            for (int s = s_begin; s < s_end; ++s) {
-                const Segment sg = a.segs[s];
+            for (int si = 0; si < s_end - s_begin; ++si) {
+                const Segment sg = a.segs[REV ? s_end - 1 - si : s_begin + si];
                 const tm_block c = a.cols[sg.col];
                 const int n = sg.k1 - sg.k0 + 2;
                 for (int q = 0; q < n; ++q, ++p) {
                     const int st_i = p % kHeatStages;
                     if (p >= kHeatStages) mbar_wait(&empty[st_i], ((p / kHeatStages) - 1) & 1);
                     issue<PACKED>(&map, &xmap, a, stages + st_i * a.stage_elems, &bars[st_i], c, comp,
-                                  c.z0 + sg.k0 - 1 + q, tx_bytes);
+                                  REV ? c.z0 + sg.k1 - q : c.z0 + sg.k0 - 1 + q, tx_bytes);
                 }
             }
         }
@@ -149,15 +149,19 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     const int nyb = a.nyv, nzb = a.nzv;
     uint32_t g = 0;  // CTA-wide plane counter of the current segment's first plane
 
-    for (int s = s_begin; s < s_end; ++s) {
-        const Segment sg = a.segs[s];
+    // REV: segments in reverse order and each column marched downward in z, so a
+    // step that follows a forward step first reads the planes that step wrote
+    // last (still in L2).  Same fluxes, same bits.
+    for (int si = 0; si < s_end - s_begin; ++si) {
+        const Segment sg = a.segs[REV ? s_end - 1 - si : s_begin + si];
         const tm_block c = a.cols[sg.col];
         const int nk = sg.k1 - sg.k0;
         const int xi = min(lane * CPL, c.nx - CPL);  // lane's first cell (clamped for idle lanes)
         const bool lane_on = lane * CPL < c.nx;
         // output rows: 64-bit row bases + one 32-bit running plane offset
         double *const obase = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp;
-        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + xi);
+        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0 + (REV ? nk - 1 : 0)) * st.plane + (int64_t)c.y0 * st.row +
+                                   c.x0 + xi);
         double *orow[RPW];
         bool on[RPW];
         uint32_t roff[RPW];  // smem byte offset of the row's first cell (rows past max_ny clamp; never stored)
@@ -217,8 +221,8 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
             }
         }
-        const uint32_t xstep = 2u * (uint32_t)nyb;
-        uint32_t xk = 0;
+        const int64_t xstep = REV ? -2 * (int64_t)nyb : 2 * (int64_t)nyb;
+        if (REV && xhp) xhp += (int64_t)(nk - 1) * 2 * nyb;  // x halo of the first plane processed
 
         // priming: planes k0-1 and k0 -> carried z flux and centre values
         double ua[RPW][CPL], ub[RPW][CPL], fzm[RPW][CPL];
@@ -230,9 +234,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
+                    // forward: s0 = plane k0-1, s1 = k0, carry fz- of k0; REV: s0 = plane k1,
+                    // s1 = k1-1, carry fz+ of k1-1 (u[k+1] - u[k] either way)
                     const double lo = lds_f64(s0 + roff[i] + 8u * j), hi = lds_f64(s1 + roff[i] + 8u * j);
                     ua[i][j] = hi;
-                    fzm[i][j] = rn_mul(rn_sub(hi, lo), c2);
+                    fzm[i][j] = REV ? rn_mul(rn_sub(lo, hi), c2) : rn_mul(rn_sub(hi, lo), c2);
                 }
         }
         release(g);
@@ -283,11 +289,13 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
                     const double u0 = cur[i][j];
-                    const double fzp = rn_mul(rn_sub(nxt[i][j], u0), c2);
+                    // fresh z flux toward the next plane; fzm[][] carries the other one
+                    const double fnew = REV ? rn_mul(rn_sub(u0, nxt[i][j]), c2) : rn_mul(rn_sub(nxt[i][j], u0), c2);
+                    const double fzp = REV ? fzm[i][j] : fnew, fzn = REV ? fnew : fzm[i][j];
                     double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
-                    sum = rn_add(sum, rn_mul(rn_sub(fzp, fzm[i][j]), c2));
+                    sum = rn_add(sum, rn_mul(rn_sub(fzp, fzn), c2));
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
-                    fzm[i][j] = fzp;
+                    fzm[i][j] = fnew;
                 }
             }
             // all shared reads of the centre plane are done: hand its stage back early
@@ -311,8 +319,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 }
             }
             if (SCATTER) {
-                if (kk == kz_lo || kk == kz_hi) {  // warp-uniform, two planes per column
-                    const int64_t zd = kk == kz_lo ? zoff_lo : zoff_hi;
+                const int kz = REV ? nk - 1 - kk : kk;  // plane index from k0
+                if (kz == kz_lo || kz == kz_hi) {  // warp-uniform, two planes per column
+                    const int64_t zd = kz == kz_lo ? zoff_lo : zoff_hi;
 #pragma unroll
                     for (int i = 0; i < RPW; ++i)
                         if (on[i]) st_cells(orow[i] + koff + zd, i);
@@ -320,11 +329,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 if (xhp) {
 #pragma unroll
                     for (int i = 0; i < RPW; ++i)
-                        if (on[i]) xhp[xk + i] = x_right ? out[i][CPL - 1] : out[i][0];
+                        if (on[i]) xhp[i] = x_right ? out[i][CPL - 1] : out[i][0];
+                    xhp += xstep;
                 }
-                xk += xstep;
             }
-            koff += pstep;
+            koff = REV ? koff - pstep : koff + pstep;
         };
         int kk = 0;
         for (; kk + 1 < nk; kk += 2) {  // ping-pong: no register rotation
@@ -603,10 +612,10 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 
 namespace {
 
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV>
 int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int nctas, int ncomp,
                      size_t smem, cudaStream_t s) {
-    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER>;
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -619,25 +628,25 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const Marc
     return TM_OK;
 }
 
-template <bool PACKED, bool SCATTER>
+template <bool PACKED, bool SCATTER, bool REV>
 int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int cpl, int rows, int nctas,
                  int ncomp, size_t smem, cudaStream_t s) {
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
-        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<2, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
     }
     if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp
-        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<4, 16, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
     }
-    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
-    return launch_march_one<1, 16, 4, PACKED, SCATTER>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
 }
 
 
@@ -772,7 +781,7 @@ int tm_march_plan_destroy(tm_march_plan *p) {
 
 int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
                   double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old, double *xh_new,
-                  const int32_t *d_nbr, void *stream) {
+                  const int32_t *d_nbr, int32_t reverse, void *stream) {
     using namespace tmk;
     if (!p) return fail(TM_ERR_INVALID, "tm_heat_march: null plan");
     int rc = check_layout(layout, "tm_heat_march");
@@ -822,9 +831,10 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
     if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
     cudaStream_t s = as_stream(stream);
-    if (!packed) return launch_march<false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    if (!scatter) return launch_march<true, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    return launch_march<true, true>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (!packed) return launch_march<false, false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (!scatter) return launch_march<true, false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (reverse) return launch_march<true, true, true>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    return launch_march<true, true, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
 }
 
 int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,

@@ -144,7 +144,7 @@ def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None 
     plan = march_plan(mf_old, False, max_rows, nctas)
     c = params.coefficients()
     _native.check(_native.load().tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
-                                               mf_old.ncomp, c[0], c[1], c[2], c[3], None, None, None,
+                                               mf_old.ncomp, c[0], c[1], c[2], c[3], None, None, None, 0,
                                                mf_old.stream()), "tm_heat_march")
 
 
@@ -256,14 +256,17 @@ class FusedHalo:
         xh = self.xh[id(mf)]
         self._init_plan.run(xh.data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
 
-    def step(self, new: MultiFab, old: MultiFab, params) -> None:
+    def step(self, new: MultiFab, old: MultiFab, params, reverse: bool = False) -> None:
         """One fused step: sweep old -> new reading old's face halos and
-        writing new's face halos (no separate FillBoundary)."""
+        writing new's face halos (no separate FillBoundary).  ``reverse``
+        walks the columns backwards (same results): alternating it between
+        consecutive steps lets each step start on the planes the previous
+        one wrote last, while they are still in L2."""
         c = params.coefficients()
         _native.check(_native.load().tm_heat_march(
             self.plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
-            self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), old.stream()),
-            "tm_heat_march(fused)")
+            self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
+            old.stream()), "tm_heat_march(fused)")
 
 
 class FusedGSRB:

@@ -78,8 +78,8 @@ class HeatRunner:
         self._primed = False
 
     def _step(self, old: MultiFab, new: MultiFab) -> None:
-        if self.fused:
-            self.fh.step(new, old, self.params)
+        if self.fused:  # b -> a steps walk backwards: they start where a -> b ended (L2)
+            self.fh.step(new, old, self.params, reverse=old is self.b)
         elif old.dm.nranks > 1:  # halo messages overlap the interior sweep
             overlapped_step(new, old, self.geom, self.params, self.plan, self.schedule, self.zmerge)
         else:

@@ -43,11 +43,13 @@ def main():
                 fh = march.FusedHalo(a, b, geom, rows, nctas)
                 fh.prime(a)
                 ms = graph_time(lambda: (fh.step(b, a, p), fh.step(a, b, p)), 10) / 2
+                msr = graph_time(lambda: (fh.step(b, a, p), fh.step(a, b, p, reverse=True)), 10) / 2
             except Exception as e:  # noqa: BLE001
                 print(f"{cfg} fused rows={rows} nctas={nctas}: {e}")
                 continue
             print(f"{cfg} fused-step rows={rows} nctas={fh.plan.nctas}: {ms * 1e3:.1f} us "
-                  f"{16 * cells / ms / 1e6:.0f} GB/s alg ({cells / ms / 1e6:.1f} G cell/s)")
+                  f"{16 * cells / ms / 1e6:.0f} GB/s alg ({cells / ms / 1e6:.1f} G cell/s); "
+                  f"alternating direction {msr * 1e3:.1f} us ({cells / msr / 1e6:.1f} G cell/s)")
 
 
 if __name__ == "__main__":
@@ -71,7 +73,7 @@ def packed_noscatter(cfg="C2", rows=16, nctas=296):
 
     def go():
         _native.check(_native.load().tm_heat_march(fh.plan.handle, a.layout.to_c(), a.ptr, b.ptr, a.ncomp, c[0], c[1],
-                                                   c[2], c[3], fh.xh[id(a)].data_ptr(), None, None, a.stream()), "m")
+                                                   c[2], c[3], fh.xh[id(a)].data_ptr(), None, None, 0, a.stream()), "m")
     ms = graph_time(go, 20)
     print(f"{cfg} packed-noscatter rows={rows} nctas={nctas}: {ms * 1e3:.1f} us")
 
