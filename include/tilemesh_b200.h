@@ -149,6 +149,24 @@ int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uo
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);
 
+/* Two heat steps per launch (temporal blocking, Kernel A3): u2 = two
+ * forward-Euler steps of u0 on every column of the plan, the intermediate
+ * field computed in shared memory on the column plus a one-cell ring.
+ * Bit-identical to two rounds of FillBoundary + tm_heat_sweep.  Columns:
+ * even width <= 64, <= 16 rows; nghost >= 2.
+ * xh_old == NULL: u0's two ghost layers are read from storage (FillBoundary
+ * must have run); only valid cells of u2 are written.
+ * xh_old != NULL: fused halo exchange for uniform boxes -- x halos from the
+ * packed buffer xh[(slot*ncomp+c)][2*(z+2)+side][y+2][2] (side 0 = x -2,-1,
+ * side 1 = x nx, nx+1; y in [-2, ny+1], z in [-2, nz+1]), y/z ghosts from
+ * storage; every u2 cell within two layers of a box face is also written to
+ * the neighbours' halos of the new field (storage y/z ghosts, xh_new): faces
+ * two deep, edges one deep -- all the next launch reads.
+ * d_nbr27[27*slot + (ox+1) + 3*(oy+1) + 9*(oz+1)] = neighbour slot, -1 = none. */
+int tm_heat_march2(tm_march_plan *plan, const tm_layout *layout, const double *u0, double *u2,
+                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
+                   const double *xh_old, double *xh_new, const int32_t *d_nbr27, void *stream);
+
 /* Fused red (0) / black (1) Gauss-Seidel pass of the column march, in place on
  * phi (ncomp 1), x halos from the packed buffer xh, and the updated colour's
  * boundary values scattered into the face neighbours' halos (phi ghost

@@ -120,8 +120,8 @@ def ctas_per_sm(mf: MultiFab, columns: np.ndarray, packed: bool, rhs_rows: bool 
 
 
 def march_plan(mf: MultiFab, packed: bool = False, max_rows: int | None = None,
-               nctas: int | None = None, rhs_rows: bool = False) -> "_native.MarchPlan":
-    key = ("march", packed, max_rows, nctas, rhs_rows, mf.layout, tuple(mf.local_units))
+               nctas: int | None = None, rhs_rows: bool = False, tag: str = "march") -> "_native.MarchPlan":
+    key = (tag, packed, max_rows, nctas, rhs_rows, mf.layout, tuple(mf.local_units))
     plan = mf._plans.get(key)
     if plan is None:
         cols = march_columns(mf, max_rows, packed)
@@ -151,6 +151,78 @@ def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None 
 # --------------------------------------------------------------------------
 # fused halo path
 # --------------------------------------------------------------------------
+def heat_march2(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None = None,
+                nctas: int | None = None, xh_old=None, xh_new=None, nbr27=None) -> None:
+    """Two heat steps in one launch (Kernel A3, tm_heat_march2): ``mf_new``
+    = two forward-Euler steps of ``mf_old``.  Without ``xh_old`` the 2+
+    ghost layers of ``mf_old`` must be filled; with packed x halos (see
+    ``FusedHalo2``) the launch also fills ``mf_new``'s halos.  Bit-identical to
+    FillBoundary + heat_step twice."""
+    if mf_old.nghost < 2:
+        raise ValueError("two-step march needs nghost >= 2")
+    if not mf_new.same_layout(mf_old):
+        raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
+    if not march_eligible(mf_old) or max(mf_old.units[u].valid.extents[0] for u in mf_old.local_units) > 64:
+        raise ValueError("two-step march needs boxes of even x extent <= 64")
+    plan = march_plan(mf_old, False, min(max_rows or 16, 16), nctas or sm_count(mf_old.device), tag="march2")
+    c = params.coefficients()
+
+    def ptr(t):
+        return None if t is None else t.data_ptr()
+
+    _native.check(_native.load().tm_heat_march2(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
+                                                mf_old.ncomp, c[0], c[1], c[2], c[3], ptr(xh_old), ptr(xh_new),
+                                                ptr(nbr27), mf_old.stream()), "tm_heat_march2")
+
+
+class FusedHalo2:
+    """Packed two-deep x halos + 27-neighbour table for a pair of nghost >= 2
+    MultiFabs stepped two steps per launch with the fused halo exchange."""
+
+    def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, nctas: int | None = None):
+        import torch
+
+        if not (two_step_eligible(a, geom) and a.same_layout(b)) or a.nghost < 2:
+            raise ValueError("layout is not eligible for the two-step fused path")
+        self.geom = geom
+        L = a.layout
+        self.nyv = L.ny - 2 * L.nghost
+        self.nzv = L.nz - 2 * L.nghost
+        shape = (L.nslots * a.ncomp, 2 * (self.nzv + 4), self.nyv + 4, 2)
+        self.xh = {id(a): torch.zeros(shape, dtype=torch.float64, device=a.device),
+                   id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
+        self.nbr = torch.as_tensor(neighbors27(a, geom).reshape(-1), dtype=torch.int32, device=a.device)
+        self.nctas = nctas
+        self._init = self._xh_init_plan(a)
+
+    def _xh_init_plan(self, mf: MultiFab):
+        """Copy tags: every slot's two x-halo sides <- its own ghost columns
+        (after a FillBoundary), rows [-2, ny+1], planes [-2, nz+1]."""
+        L = mf.layout
+        ng, ny4, nz4 = mf.nghost, self.nyv + 4, self.nzv + 4
+        tags = np.zeros(2 * L.nslots, dtype=_native.COPY_TAG_DTYPE)
+        for s, u in enumerate(mf.local_units):
+            nx = mf.units[u].valid.extents[0]
+            for side in (0, 1):
+                src = s * L.slot + (ng - 2) * L.plane + (ng - 2) * L.row + (L.xoff - 2 if side == 0 else L.xoff + nx)
+                dst = ((s * mf.ncomp) * 2 * nz4 + side) * ny4 * 2
+                tags[2 * s + side] = (dst, src, 2, ny4, nz4, 0)
+        self.xh_side = (2, 4 * ny4, 4 * ny4 * nz4)
+        return _native.CopyPlan(tags, mf.ncomp)
+
+    def prime(self, mf: MultiFab, plan=None) -> None:
+        """Fill every ghost of ``mf`` (FillBoundary) and its packed x halos."""
+        from .multifab import fill_boundary
+
+        fill_boundary(mf, self.geom, plan)
+        self._init.run(self.xh[id(mf)].data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
+
+    def step2(self, new: MultiFab, old: MultiFab, params) -> None:
+        """Two fused steps: old -> new, halos of new filled for the next launch."""
+        heat_march2(new, old, params, nctas=self.nctas, xh_old=self.xh[id(old)], xh_new=self.xh[id(new)],
+                    nbr27=self.nbr)
+
+
 def face_neighbors(mf: MultiFab, geom: Geometry):
     """Per local slot, the slots of the 6 face neighbours (-x,+x,-y,+y,-z,+z),
     or None when the layout is not fusable: every face must be covered by
@@ -196,6 +268,63 @@ def fusable(mf: MultiFab, geom: Geometry) -> bool:
     if ny % 2 or (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
         return False
     return face_neighbors(mf, geom) is not None
+
+
+def neighbors27(mf: MultiFab, geom: Geometry):
+    """Per local slot, the slot of the box at every offset (ox, oy, oz) in
+    {-1,0,1}^3 (index (ox+1) + 3*(oy+1) + 9*(oz+1); the centre is the slot
+    itself), or None unless every such neighbour is one LOCAL box of
+    identical extents (uniform chopped domains, periodic or interior)."""
+    valids = [u.valid for u in mf.units]
+    index = BoxIndex(valids)
+    dom = geom.domain
+    n = dom.extents
+    table = np.full((len(mf.local_units), 27), -1, dtype=np.int32)
+    for s, u in enumerate(mf.local_units):
+        v = valids[u]
+        e = v.extents
+        for oz in (-1, 0, 1):
+            for oy in (-1, 0, 1):
+                for ox in (-1, 0, 1):
+                    o = (ox, oy, oz)
+                    img = []
+                    for d in range(3):
+                        lo = v.lo[d] + o[d] * e[d]
+                        if not (dom.lo[d] <= lo and lo + e[d] - 1 <= dom.hi[d]):
+                            if not geom.periodic[d]:
+                                return None
+                            lo = dom.lo[d] + (lo - dom.lo[d]) % n[d]
+                        img.append(lo)
+                    target = Box(img, [img[k] + e[k] - 1 for k in range(3)])
+                    hits = index.query(target)
+                    if len(hits) != 1 or valids[hits[0]] != target or hits[0] not in mf.slot_of:
+                        return None
+                    table[s, (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)] = mf.slot_of[hits[0]]
+    return table
+
+
+def two_step_eligible(mf: MultiFab, geom: Geometry) -> bool:
+    """Layouts the fused two-steps-per-launch path supports: uniform boxes of
+    width a multiple of 8 up to 64, y and z extents >= 4, every neighbour
+    (faces, edges, corners) a local box."""
+    if not mf.local_units or comm_info_world(mf) != 1:
+        return False
+    ext = {mf.units[u].valid.extents for u in mf.local_units}
+    if len(ext) != 1:
+        return False
+    (nx, ny, nz), = ext
+    if nx % 8 or nx > 64 or ny < 4 or nz < 4:
+        return False
+    L = mf.layout
+    if (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
+        return False
+    return neighbors27(mf, geom) is not None
+
+
+def comm_info_world(mf: MultiFab) -> int:
+    from .multifab import comm_info
+
+    return comm_info()[1]
 
 
 def xh_init_plan(mf: MultiFab, table, nyv: int, nzv: int):

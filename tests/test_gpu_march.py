@@ -155,3 +155,52 @@ def test_fused_reverse_direction_matches_oracle(tm, cfg, n, mgs, steps, rows, nc
         a, b = b, a
     tm.fill_boundary(a, geom)
     assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
+
+
+@pytest.mark.parametrize("cfg,n,mgs,steps,nctas", [
+    ("C2", 64, 32, 2, None),
+    ("C2", 64, 32, 4, 7),      # segments crossing columns
+    ("C2", 96, 48, 2, None),   # 48-wide boxes: idle lanes, 16-row columns of 48-row boxes
+    ("C5", 64, 32, 2, 5),      # 2 components, 32-wide (1 cell per lane)
+    ("C1", 40, 20, 2, None),   # 20-wide boxes, columns of 16 + 4 rows
+])
+def test_two_step_march_matches_oracle(tm, cfg, n, mgs, steps, nctas):
+    import dataclasses
+
+    from paper_1604_03570_b200.march import heat_march2
+
+    w = dataclasses.replace(tm.CONFIGS[cfg].scaled(n, mgs, steps), nghost=2)
+    geom, ba, glob, a = setup(tm, w)
+    b = a.clone_empty()
+    p = tm.HeatParams.stable(1.0, geom.dx)
+    plan = tm.build_fill_plan(a, geom)
+    for _ in range(steps // 2):
+        tm.fill_boundary(a, geom, plan)
+        heat_march2(b, a, p, nctas=nctas)
+        a, b = b, a
+    assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
+
+
+@pytest.mark.parametrize("cfg,n,mgs,steps,nctas", [
+    ("C2", 64, 32, 6, None),
+    ("C2", 64, 16, 4, 7),       # 16-wide boxes, segments crossing columns
+    ("C5", 64, 32, 4, None),    # 2 components
+    ("C1", 48, 24, 4, 5),       # 24-wide boxes: columns of 16 + 8 rows
+])
+def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas):
+    """Consecutive two-step launches with the fused ghost scatter (no
+    FillBoundary in between) give the oracle's bits."""
+    import dataclasses
+
+    from paper_1604_03570_b200.march import FusedHalo2
+
+    w = dataclasses.replace(tm.CONFIGS[cfg].scaled(n, mgs, steps), nghost=2)
+    geom, ba, glob, a = setup(tm, w)
+    b = a.clone_empty()
+    p = tm.HeatParams.stable(1.0, geom.dx)
+    fh = FusedHalo2(a, b, geom, nctas)
+    fh.prime(a)
+    for _ in range(steps // 2):
+        fh.step2(b, a, p)
+        a, b = b, a
+    assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
