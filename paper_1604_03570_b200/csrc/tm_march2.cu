@@ -56,7 +56,7 @@ struct March2Args {
 };
 
 template <int CPL, int NWARP, bool PACKED>
-__global__ void __launch_bounds__((NWARP + 1) * 32, 1)
+__global__ void __launch_bounds__(NWARP * 32, 1)
     march2_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap xmap,
                   March2Args a) {
     using namespace tmk;
@@ -64,7 +64,6 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     double *stages = reinterpret_cast<double *>(smem_raw);
     double *u1s = stages + (size_t)kStages2 * a.stage_elems;
     uint64_t *bars = reinterpret_cast<uint64_t *>(u1s + (size_t)kU1Slots * a.u1_elems);
-    uint64_t *empty = bars + kStages2;
 
     const int comp = blockIdx.y;
     const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
@@ -73,58 +72,55 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     const int bx = a.box_x, by = a.box_y, ux = a.u1_x;
     const uint32_t tx_bytes = (uint32_t)((bx * by + (PACKED ? 4 * by : 0)) * (int)sizeof(double));
 
+    // No producer warp: the per-plane CTA barrier already orders every stage's last
+    // read before its refill, so thread 0 issues the TMA loads right after each
+    // barrier, up to three planes ahead of the one being consumed.  16 warps with
+    // no 17th keep 4 warps per scheduler and 128 registers per thread.
+    const int g_ng0 = a.L.nghost;
+    int ps = s_begin, pq = 0;  // producer cursor: segment, plane within it
+    uint32_t pnext = 0;        // next plane (CTA sequence) to issue
+    auto issue_upto = [&](uint32_t last) {
+        fence_proxy_async_shared();  // generic-proxy reads of the stages before their async refill
+        while (pnext <= last && ps < s_end) {
+            const Segment sg = a.segs[ps];
+            const tm_block c = a.cols[sg.col];
+            const int w = c.slot * a.L.ncomp + comp;
+            const uint32_t st_i = pnext & (kStages2 - 1);
+            double *stage = stages + st_i * a.stage_elems;
+            const int z = c.z0 + sg.k0 - 2 + pq;
+            mbar_arrive_expect_tx(&bars[st_i], tx_bytes);
+            if (PACKED) {
+                tma_load_plane(stage, &map, &bars[st_i], c.x0, c.y0 - 2, z, w);
+                // x halos: rows [y0-2, y0+ny+2) of a plane-side are one contiguous run
+                const int zh = 2 * (z - g_ng0 + 2), yh = c.y0 - g_ng0;
+                tma_load_plane(stage + a.xh_off, &xmap, &bars[st_i], 2 * yh, zh, 0, w);
+                tma_load_plane(stage + a.xh1_off, &xmap, &bars[st_i], 2 * yh, zh + 1, 0, w);
+            } else {
+                tma_load_plane(stage, &map, &bars[st_i], c.x0 - 2, c.y0 - 2, z, w);
+            }
+            ++pnext;
+            if (++pq == sg.k1 - sg.k0 + 4) {
+                pq = 0;
+                ++ps;
+            }
+        }
+    };
     if (tid == 0) {
         prefetch_tensormap(&map);
         if (PACKED) prefetch_tensormap(&xmap);
 #pragma unroll
-        for (int s = 0; s < kStages2; ++s) {
-            mbar_init(&bars[s], 1);
-            mbar_init(&empty[s], NWARP);
-        }
+        for (int s = 0; s < kStages2; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
+        issue_upto(kStages2 - 1);
     }
     __syncthreads();
 
-    if (warp == NWARP) {  // ---------------- producer warp ----------------
-        if (lane == 0) {
-            const int g_ng = a.L.nghost;
-            uint32_t p = 0;
-            for (int s = s_begin; s < s_end; ++s) {
-                const Segment sg = a.segs[s];
-                const tm_block c = a.cols[sg.col];
-                const int w = c.slot * a.L.ncomp + comp;
-                const int n = sg.k1 - sg.k0 + 4;
-                for (int q = 0; q < n; ++q, ++p) {
-                    const uint32_t st_i = p & (kStages2 - 1);
-                    if (p >= (uint32_t)kStages2) mbar_wait(&empty[st_i], ((p / kStages2) - 1) & 1);
-                    double *stage = stages + st_i * a.stage_elems;
-                    const int z = c.z0 + sg.k0 - 2 + q;
-                    mbar_arrive_expect_tx(&bars[st_i], tx_bytes);
-                    if (PACKED) {
-                        tma_load_plane(stage, &map, &bars[st_i], c.x0, c.y0 - 2, z, w);
-                        // x halos: rows [y0-2, y0+ny+2) of a plane-side are one contiguous run
-                        const int zh = 2 * (z - g_ng + 2), yh = c.y0 - g_ng;
-                        tma_load_plane(stage + a.xh_off, &xmap, &bars[st_i], 2 * yh, zh, 0, w);
-                        tma_load_plane(stage + a.xh1_off, &xmap, &bars[st_i], 2 * yh, zh + 1, 0, w);
-                    } else {
-                        tma_load_plane(stage, &map, &bars[st_i], c.x0 - 2, c.y0 - 2, z, w);
-                    }
-                }
-            }
-        }
-        return;
-    }
-
     // ---------------- consumer warps ----------------
     const uint32_t sbase = smem_u32(stages), ubase = smem_u32(u1s);
-    const uint32_t bfull = smem_u32(bars), bempty = smem_u32(empty);
+    const uint32_t bfull = smem_u32(bars);
     const uint32_t sbytes = (uint32_t)a.stage_elems * 8u, ubytes = (uint32_t)a.u1_elems * 8u;
     auto saddr = [&](uint32_t q) { return sbase + (q & (kStages2 - 1)) * sbytes; };
     auto wait_plane = [&](uint32_t q) { mbar_wait_u32(bfull + (q & (kStages2 - 1)) * 8u, (q / kStages2) & 1u); };
-    auto release = [&](uint32_t q) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive_u32(bempty + (q & (kStages2 - 1)) * 8u);
-    };
     const double c0 = a.c0, c1 = a.c1, c2 = a.c2, c3 = a.c3;
     const Strides st = strides_of(a.L);
     const uint32_t ys0 = (uint32_t)bx * 8u, ys1 = (uint32_t)ux * 8u;  // row strides (bytes): u0 main, u1 slot
@@ -243,7 +239,6 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
                 f0[j] = rn_mul(rn_sub(u0c[j], lds_f64(sA + o0 + 8u * j)), c2);
             }
             if (has_ring) f0r = rn_mul(rn_sub(lds_f64(sB + rcc), lds_f64(sA + rcc)), c2);
-            release(g);
         }
         for (int j = 0; j < nk + 2; ++j) {
             // ---- u1 at plane k0-1+j: centre stage g+1+j, next stage g+2+j ----
@@ -289,7 +284,6 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
                 vr = point(sc, rcc, rxm, rxp, rym, ryp, f0r, lds_f64(sn + rcc), fz);
                 f0r = fz;
             }
-            release(qc);
 #pragma unroll
             for (int jj = 0; jj < CPL; ++jj) u0c[jj] = nxt[jj];
             // publish u1(k0-1+j); rows >= ny and lanes past nx hold values nobody reads
@@ -301,6 +295,8 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
             }
             if (has_ring) sts_f64(us + o1r, vr);
             named_barrier_sync(1, NWARP * 32);
+            // every warp is done with planes <= qc: refill up to qn + 3
+            if (tid == 0) issue_upto(qn + 3);
             if (j == 0) {
 #pragma unroll
                 for (int jj = 0; jj < CPL; ++jj) u1c[jj] = u1n[jj];
@@ -402,7 +398,6 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
             if (xq0) xq0 += xzstep;
             if (xq1) xq1 += xzstep;
         }
-        release(g + (uint32_t)nk + 3);
         g += (uint32_t)nk + 4;
         gj += (uint32_t)nk + 2;
     }
@@ -418,7 +413,7 @@ int launch_march2_one(const CUtensorMap &map, const CUtensorMap &xmap, const Mar
         if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(march2)");
         configured = true;
     }
-    kern<<<dim3(nctas, ncomp), (NWARP + 1) * 32, smem, s>>>(map, xmap, a);
+    kern<<<dim3(nctas, ncomp), NWARP * 32, smem, s>>>(map, xmap, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march2 launch");
     return TM_OK;
@@ -470,7 +465,7 @@ int tm_heat_march2(tm_march_plan *p, const tm_layout *layout, const double *u0, 
     a.nyb = L.ny - 2 * L.nghost;
     a.nzb = L.nz - 2 * L.nghost;
     const size_t smem = ((size_t)kStages2 * a.stage_elems + (size_t)kU1Slots * a.u1_elems) * sizeof(double) +
-                        2 * kStages2 * sizeof(uint64_t);
+                        kStages2 * sizeof(uint64_t);
     CUtensorMap map, xmap;
     rc = encode_plane_map(&map, L, u0, a.box_x, a.box_y);
     if (rc) return rc;
