@@ -21,6 +21,9 @@
 // Two halo modes:
 //   STD    -- u0's two ghost layers are read from storage (the caller fills
 //             them, nghost >= 2); only valid cells of u2 are written.
+//   STORE  -- fused halo exchange through storage ghosts: as STD, and the
+//             epilogue writes the neighbours' ghost cells of the new field
+//             (faces two deep, edges one deep), x ghosts as full 64-B chunks.
 //   PACKED -- fused halo exchange.  x halos come from a dense buffer
 //             xh[w][2*(z+2)+side][y+2][2] (w = slot*ncomp+c, side 0 = x -2,-1,
 //             side 1 = x nx, nx+1, y in [-2, ny+1], z in [-2, nz+1]); y/z
@@ -55,11 +58,13 @@ struct March2Args {
     int32_t nxb, nyb, nzb;              // PACKED: valid extents of every box
 };
 
-template <int CPL, int NWARP, bool PACKED>
-__global__ void __launch_bounds__(NWARP * 32, 1)
+template <int CPL, int NWARP, int HALO>
+__global__ void __launch_bounds__(NWARP * 32, NWARP <= 8 ? 2 : 1)
     march2_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant__ CUtensorMap xmap,
                   March2Args a) {
     using namespace tmk;
+    constexpr bool PACKED = HALO == 1;  // x halos from / to the packed buffers
+    constexpr bool SCAT = HALO != 0;    // fused halo exchange (scatter into the new field)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
     double *u1s = stages + (size_t)kStages2 * a.stage_elems;
@@ -192,10 +197,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
         double *const orow = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)r * st.row;
         uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + xi);
         // PACKED scatter: y layer of this row (per warp), x-halo roles of this lane
-        const int32_t *nb = PACKED ? a.nbr27 + 27 * c.slot : nullptr;
+        const int32_t *nb = SCAT ? a.nbr27 + 27 * c.slot : nullptr;
         const int yv = c.y0 - g_ng + r;  // valid y of this row
         int oyv = 0, ylay = 3;
-        if (PACKED) {
+        if (SCAT) {
             if (yv < 2) {
                 oyv = -1;
                 ylay = yv + 1;
@@ -224,6 +229,27 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
             }
         }
         const int64_t xzstep = 4 * (int64_t)(a.nyb + 4);  // next z of the same side
+        // HALO 2 (storage ghosts): x halos as 64-B chunks -- the lanes holding cells [0, 8)
+        // write the -x box's columns [nx, nx+8) (ghosts + row padding), those holding
+        // [nx-8, nx) the +x box's columns [-8, 0); face rows and (x, y) edge rows
+        const bool cl = HALO == 2 && xi < 8 && lane * CPL < c.nx, cr = HALO == 2 && xi + CPL > a.nxb - 8 && lane * CPL < c.nx;
+        int64_t dl0 = 0, dl1 = 0, dr0 = 0, dr1 = 0;
+        bool vl0 = false, vl1 = false, vr0 = false, vr1 = false;
+        if (HALO == 2) {
+            const int TL = nb[12], TR = nb[14];
+            vl0 = cl && TL >= 0;
+            vr0 = cr && TR >= 0;
+            dl0 = (int64_t)(TL - c.slot) * st.slot + a.nxb;
+            dr0 = (int64_t)(TR - c.slot) * st.slot - a.nxb;
+            if (oyv != 0 && ylay == 1) {
+                const int TL1 = nb[12 + 3 * oyv], TR1 = nb[14 + 3 * oyv];
+                const int64_t dy = -(int64_t)oyv * a.nyb * st.row;
+                vl1 = cl && TL1 >= 0;
+                vr1 = cr && TR1 >= 0;
+                dl1 = (int64_t)(TL1 - c.slot) * st.slot + dy + a.nxb;
+                dr1 = (int64_t)(TR1 - c.slot) * st.slot + dy - a.nxb;
+            }
+        }
 
         // u0 march state (main cells: centre values + carried z flux; ring cell: carried flux)
         double u0c[CPL], f0[CPL], f0r = 0.0;
@@ -353,7 +379,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
             };
             if (on) {
                 put(0);
-                if (PACKED && a.xh_new) {
+                if (SCAT && (HALO == 2 || a.xh_new)) {
                     const int zv = zv0 + j - 2;
                     int ozv = 0, zlay = 3;
                     if (zv < 2) {
@@ -376,6 +402,23 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
                         if (ozv != 0 && zlay == 1) {  // two planes per column
                             const int T2 = nb[(xside ? 12 : 14) + 9 * ozv];
                             if (T2 >= 0) xput(xh_ptr(T2, 0, ozv, zv));
+                        }
+                    }
+                    if (HALO == 2) {
+                        if (vl0) put(dl0);
+                        if (vr0) put(dr0);
+                        if (vl1) put(dl1);
+                        if (vr1) put(dr1);
+                        if (ozv != 0 && zlay == 1 && (cl || cr)) {  // (x, z) edges: two planes per column
+                            const int T2 = nb[(cl ? 12 : 14) + 9 * ozv];
+                            if (T2 >= 0)
+                                put((int64_t)(T2 - c.slot) * st.slot - (int64_t)ozv * a.nzb * st.plane +
+                                    (cl ? a.nxb : -a.nxb));
+                            if (cl && cr) {  // narrow boxes: the lane feeds both sides
+                                const int T3 = nb[14 + 9 * ozv];
+                                if (T3 >= 0)
+                                    put((int64_t)(T3 - c.slot) * st.slot - (int64_t)ozv * a.nzb * st.plane - a.nxb);
+                            }
                         }
                     }
                     // y / z ghost rows of the neighbours: faces two deep, the (y, z) edge one deep
@@ -403,10 +446,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     }
 }
 
-template <int CPL, int NWARP, bool PACKED>
+template <int CPL, int NWARP, int HALO>
 int launch_march2_one(const CUtensorMap &map, const CUtensorMap &xmap, const March2Args &a, int nctas, int ncomp,
                       size_t smem, cudaStream_t s) {
-    auto kern = march2_kernel<CPL, NWARP, PACKED>;
+    auto kern = march2_kernel<CPL, NWARP, HALO>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -417,6 +460,17 @@ int launch_march2_one(const CUtensorMap &map, const CUtensorMap &xmap, const Mar
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march2 launch");
     return TM_OK;
+}
+
+template <int HALO>
+int launch_mode(const CUtensorMap &map, const CUtensorMap &xmap, const March2Args &a, const tm_march_plan *p,
+                int ncomp, size_t smem, cudaStream_t s) {
+    if (p->max_ny <= 8) {  // 8-row columns: two CTAs per SM
+        if (p->max_nx <= 32) return launch_march2_one<1, 8, HALO>(map, xmap, a, p->nctas, ncomp, smem, s);
+        return launch_march2_one<2, 8, HALO>(map, xmap, a, p->nctas, ncomp, smem, s);
+    }
+    if (p->max_nx <= 32) return launch_march2_one<1, 16, HALO>(map, xmap, a, p->nctas, ncomp, smem, s);
+    return launch_march2_one<2, 16, HALO>(map, xmap, a, p->nctas, ncomp, smem, s);
 }
 
 }  // namespace
@@ -433,8 +487,7 @@ int tm_heat_march2(tm_march_plan *p, const tm_layout *layout, const double *u0, 
     const tm_layout &L = *layout;
     const bool packed = xh_old != nullptr;
     if (!u0 || !u2 || u0 == u2) return fail(TM_ERR_INVALID, "tm_heat_march2: needs distinct input/output fields");
-    if (L.nghost < 2 || (packed && xh_new && !d_nbr27))
-        return fail(TM_ERR_INVALID, "tm_heat_march2: needs nghost >= 2 (and xh_new + neighbours when packed)");
+    if (L.nghost < 2) return fail(TM_ERR_INVALID, "tm_heat_march2: needs nghost >= 2");
     if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march2: bad ncomp");
     if (strides_of(L).comp >= ((int64_t)1 << 32))
         return fail(TM_ERR_INVALID, "tm_heat_march2: one component of a slot must hold < 2^32 doubles");
@@ -470,9 +523,12 @@ int tm_heat_march2(tm_march_plan *p, const tm_layout *layout, const double *u0, 
     rc = encode_plane_map(&map, L, u0, a.box_x, a.box_y);
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
+    if (packed || d_nbr27) {
+        if (a.nyb < 4 || a.nzb < 4 || a.nxb < 8 || a.nxb % 8)
+            return fail(TM_ERR_INVALID, "tm_heat_march2: fused halos need box width % 8 == 0 and y, z extents >= 4");
+        if (!d_nbr27) return fail(TM_ERR_INVALID, "tm_heat_march2: fused halos need the neighbour table");
+    }
     if (packed) {
-        if (a.nyb < 4 || a.nzb < 4 || a.nxb < 4)
-            return fail(TM_ERR_INVALID, "tm_heat_march2: packed halos need boxes of at least 4 cells per side");
         // x halos as (2*(ny+4) doubles of a plane-side, 2*(nz+4) plane-sides, 1, slot*ncomp):
         // a column's rows are one contiguous 2*box_y run
         tm_layout X{};
@@ -483,12 +539,11 @@ int tm_heat_march2(tm_march_plan *p, const tm_layout *layout, const double *u0, 
         X.nz = 1;
         rc = encode_plane_map(&xmap, X, xh_old, 2 * a.box_y, 1);
         if (rc) return rc;
-        if (p->max_nx <= 32) return launch_march2_one<1, 16, true>(map, xmap, a, p->nctas, ncomp_sweep, smem, s);
-        return launch_march2_one<2, 16, true>(map, xmap, a, p->nctas, ncomp_sweep, smem, s);
+        return launch_mode<1>(map, xmap, a, p, ncomp_sweep, smem, s);
     }
     xmap = map;
-    if (p->max_nx <= 32) return launch_march2_one<1, 16, false>(map, xmap, a, p->nctas, ncomp_sweep, smem, s);
-    return launch_march2_one<2, 16, false>(map, xmap, a, p->nctas, ncomp_sweep, smem, s);
+    if (d_nbr27) return launch_mode<2>(map, xmap, a, p, ncomp_sweep, smem, s);
+    return launch_mode<0>(map, xmap, a, p, ncomp_sweep, smem, s);
 }
 
 }  // extern "C"

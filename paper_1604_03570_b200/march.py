@@ -179,7 +179,8 @@ class FusedHalo2:
     """Packed two-deep x halos + 27-neighbour table for a pair of nghost >= 2
     MultiFabs stepped two steps per launch with the fused halo exchange."""
 
-    def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, nctas: int | None = None):
+    def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, nctas: int | None = None,
+                 max_rows: int | None = None, packed: bool = False):
         import torch
 
         if not (two_step_eligible(a, geom) and a.same_layout(b)) or a.nghost < 2:
@@ -193,6 +194,8 @@ class FusedHalo2:
                    id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
         self.nbr = torch.as_tensor(neighbors27(a, geom).reshape(-1), dtype=torch.int32, device=a.device)
         self.nctas = nctas
+        self.max_rows = max_rows
+        self.packed = packed  # x halos in dense buffers (else storage ghost columns)
         self._init = self._xh_init_plan(a)
 
     def _xh_init_plan(self, mf: MultiFab):
@@ -215,12 +218,16 @@ class FusedHalo2:
         from .multifab import fill_boundary
 
         fill_boundary(mf, self.geom, plan)
-        self._init.run(self.xh[id(mf)].data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
+        if self.packed:
+            self._init.run(self.xh[id(mf)].data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
 
     def step2(self, new: MultiFab, old: MultiFab, params) -> None:
         """Two fused steps: old -> new, halos of new filled for the next launch."""
-        heat_march2(new, old, params, nctas=self.nctas, xh_old=self.xh[id(old)], xh_new=self.xh[id(new)],
-                    nbr27=self.nbr)
+        if self.packed:
+            heat_march2(new, old, params, max_rows=self.max_rows, nctas=self.nctas, xh_old=self.xh[id(old)],
+                        xh_new=self.xh[id(new)], nbr27=self.nbr)
+        else:
+            heat_march2(new, old, params, max_rows=self.max_rows, nctas=self.nctas, nbr27=self.nbr)
 
 
 def face_neighbors(mf: MultiFab, geom: Geometry):

@@ -181,13 +181,15 @@ def test_two_step_march_matches_oracle(tm, cfg, n, mgs, steps, nctas):
     assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
 
 
-@pytest.mark.parametrize("cfg,n,mgs,steps,nctas", [
-    ("C2", 64, 32, 6, None),
-    ("C2", 64, 16, 4, 7),       # 16-wide boxes, segments crossing columns
-    ("C5", 64, 32, 4, None),    # 2 components
-    ("C1", 48, 24, 4, 5),       # 24-wide boxes: columns of 16 + 8 rows
+@pytest.mark.parametrize("packed", [False, True])
+@pytest.mark.parametrize("cfg,n,mgs,steps,nctas,rows", [
+    ("C2", 64, 32, 6, None, None),
+    ("C2", 64, 16, 4, 7, None),     # 16-wide boxes, segments crossing columns
+    ("C5", 64, 32, 4, None, 8),     # 2 components, 8-row columns
+    ("C1", 48, 24, 4, 5, None),     # 24-wide boxes: columns of 16 + 8 rows
+    ("C1", 32, 8, 4, 40, 8),        # 8-wide boxes: one lane feeds both x sides
 ])
-def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas):
+def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas, rows, packed):
     """Consecutive two-step launches with the fused ghost scatter (no
     FillBoundary in between) give the oracle's bits."""
     import dataclasses
@@ -198,7 +200,7 @@ def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas):
     geom, ba, glob, a = setup(tm, w)
     b = a.clone_empty()
     p = tm.HeatParams.stable(1.0, geom.dx)
-    fh = FusedHalo2(a, b, geom, nctas)
+    fh = FusedHalo2(a, b, geom, nctas, rows, packed)
     fh.prime(a)
     for _ in range(steps // 2):
         fh.step2(b, a, p)

@@ -16,6 +16,7 @@ from tools.sweep_shapes import graph_time  # noqa: E402
 def main():
     cfg = sys.argv[sys.argv.index("--config") + 1] if "--config" in sys.argv else "C2"
     nctas = int(sys.argv[sys.argv.index("--nctas") + 1]) if "--nctas" in sys.argv else None
+    rows = int(sys.argv[sys.argv.index("--rows") + 1]) if "--rows" in sys.argv else None
     w = dataclasses.replace(tm.CONFIGS[cfg], nghost=max(2, tm.CONFIGS[cfg].nghost))
     geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
     a = tm.MultiFab(tm.BoxArray.chop(w.domain, w.max_grid_size), w.ncomp, w.nghost)
@@ -25,15 +26,13 @@ def main():
     plan = tm.build_fill_plan(a, geom)
     tm.fill_boundary(a, geom, plan)
     cells = w.cells * w.ncomp
-    kern = graph_time(lambda: heat_march2(b, a, p, nctas=nctas), 10)
+    kern = graph_time(lambda: heat_march2(b, a, p, max_rows=rows, nctas=nctas), 10)
     fb = graph_time(lambda: tm.fill_boundary(a, geom, plan), 10)
-    pair = graph_time(lambda: (tm.fill_boundary(a, geom, plan), heat_march2(b, a, p, nctas=nctas),
-                               tm.fill_boundary(b, geom, plan), heat_march2(a, b, p, nctas=nctas)), 5) / 2
-    fh = FusedHalo2(a, b, geom, nctas)
+    pair = graph_time(lambda: (tm.fill_boundary(a, geom, plan), heat_march2(b, a, p, max_rows=rows, nctas=nctas),
+                               tm.fill_boundary(b, geom, plan), heat_march2(a, b, p, max_rows=rows, nctas=nctas)), 5) / 2
+    fh = FusedHalo2(a, b, geom, nctas, rows, packed="--packed" in sys.argv)
     fh.prime(a, plan)
     fused = graph_time(lambda: (fh.step2(b, a, p), fh.step2(a, b, p)), 5) / 2
-    noscat = graph_time(lambda: heat_march2(b, a, p, nctas=nctas, xh_old=fh.xh[id(a)]), 10)
-    print(f"{cfg} packed halos, no scatter {noscat * 1e3:.1f} us per launch")
     print(f"{cfg} fused two-step launch (scatter) {fused * 1e3:.1f} us = {fused * 1e3 / 2:.1f} us/step, "
           f"{2 * cells / fused / 1e6:.1f} G cell-upd/s")
     print(f"{cfg} two-step kernel {kern * 1e3:.1f} us ({2 * cells / kern / 1e6:.1f} G cell-upd/s, "
