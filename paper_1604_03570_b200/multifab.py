@@ -18,6 +18,7 @@ of ``libtilemesh_b200.so`` launched on the current torch stream.
 
 from __future__ import annotations
 
+
 import warnings
 from typing import Callable, NamedTuple
 
