@@ -175,6 +175,24 @@ int tm_heat_march2(tm_march_plan *plan, const tm_layout *layout, const double *u
 int tm_gsrb_march(tm_march_plan *plan, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,
                   const double *rhs, int32_t color, double h2, double *xh, const int32_t *d_nbr, void *stream);
 
+/* ---- GSRB on colour-split storage (during a solve) ---------------------------
+ * Each colour of phi in its own array [slot][z+1][y+1][i+2] (rows nx/2 + 4
+ * doubles; entry i of row (y, z) = cell x = 2i + ((c + parity + y + z) & 1),
+ * i in [-1, nx/2]), rhs split into [slot][z][y][nx/2] per colour.  A colour
+ * pass reads only the other colour and writes only its own: 24 bytes per
+ * UPDATED cell.  Same per-cell form as tm_gsrb_color (bit-identical); the
+ * pass also fills the face neighbours' ghost entries of its colour.
+ * d_parity[slot] = (x_lo + y_lo + z_lo) & 1 of each box; uniform boxes,
+ * nx % 4 == 0. */
+int tm_gsrb_split(const tm_layout *phi_layout, const double *phi, int32_t nx, int32_t ny, int32_t nz,
+                  const int32_t *d_parity, double *c0, double *c1, const tm_layout *rhs_layout, const double *rhs,
+                  double *r0, double *r1, void *stream);
+int tm_gsrb_merge(const tm_layout *phi_layout, double *phi, int32_t nx, int32_t ny, int32_t nz,
+                  const int32_t *d_parity, const double *c0, const double *c1, void *stream);
+int tm_gsrb_split_pass(tm_march_plan *plan, int32_t nslots, int32_t nx, int32_t ny, int32_t nz, int32_t color,
+                       double h2, const double *other, double *cur, const double *rhs_c, const int32_t *d_nbr,
+                       void *stream);
+
 /* ---- 9-point 8th-order Laplacian step ("wide4", Kernel W) -------------------
  * Replaces compiled.wide4_tiles / wide4_range (compiled.py:102-141) as driven
  * by kernels.wide4_step (kernels.py:218-247) and loop_wide4_step

@@ -477,3 +477,78 @@ class FusedGSRB:
         from .multifab import fill_boundary
 
         fill_boundary(self.phi, self.geom, plan)
+
+
+def split_eligible(phi: MultiFab, rhs: MultiFab, geom: Geometry) -> bool:
+    """Colour-split GSRB: the fused layout rules, x extent a multiple of 4, and
+    even periodic domain extents (a periodic image keeps its colour)."""
+    if not fusable(phi, geom) or phi.ncomp != 1 or rhs.ncomp != 1 or phi.nghost != 1:
+        return False
+    if phi.ba != rhs.ba or phi.local_units != rhs.local_units:
+        return False
+    nx = phi.units[phi.local_units[0]].valid.extents[0]
+    if nx % 4 or nx > 128:
+        return False
+    n = geom.domain.extents
+    return all(n[d] % 2 == 0 for d in range(3) if geom.periodic[d])
+
+
+class SplitGSRB:
+    """GSRB sweeps on colour-split storage: ``prime`` splits phi (after a
+    FillBoundary) and rhs into per-colour arrays, each colour pass is one
+    launch reading only the other colour (and filling the face ghosts of its
+    own), ``finalize`` merges back into phi and runs FillBoundary.
+    Bit-identical to ``stencil.gsrb_sweep``."""
+
+    def __init__(self, phi: MultiFab, rhs: MultiFab, geom: Geometry, max_rows: int | None = None,
+                 nctas: int | None = None):
+        import torch
+
+        if not split_eligible(phi, rhs, geom):
+            raise ValueError("layout is not eligible for the colour-split GSRB path")
+        self.phi, self.rhs, self.geom = phi, rhs, geom
+        v = phi.units[phi.local_units[0]].valid
+        self.nx, self.ny, self.nz = v.extents
+        nh, n = self.nx // 2, len(phi.local_units)
+        dev = phi.device
+        self.c = [torch.zeros((n, self.nz + 2, self.ny + 2, nh + 4), dtype=torch.float64, device=dev)
+                  for _ in range(2)]
+        self.r = [torch.zeros((n, self.nz, self.ny, nh), dtype=torch.float64, device=dev) for _ in range(2)]
+        par = [sum(phi.units[u].valid.lo) & 1 for u in phi.local_units]
+        self.parity = torch.as_tensor(par, dtype=torch.int32, device=dev)
+        self.nbr = torch.as_tensor(face_neighbors(phi, geom).reshape(-1), dtype=torch.int32, device=dev)
+        rows = max_rows or 16
+        self.plan = march_plan(phi, False, rows, nctas or 2 * sm_count(dev), tag="gsrb_split")
+        self.h2 = geom.dx[0] * geom.dx[0]
+        self._graph = None
+
+    def prime(self, plan=None) -> None:
+        from .multifab import fill_boundary
+
+        phi, rhs = self.phi, self.rhs
+        fill_boundary(phi, self.geom, plan)
+        _native.check(_native.load().tm_gsrb_split(
+            phi.layout.to_c(), phi.ptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
+            self.c[1].data_ptr(), rhs.layout.to_c(), rhs.ptr, self.r[0].data_ptr(), self.r[1].data_ptr(),
+            phi.stream()), "tm_gsrb_split")
+
+    def colour(self, color: int) -> None:
+        _native.check(_native.load().tm_gsrb_split_pass(
+            self.plan.handle, len(self.phi.local_units), self.nx, self.ny, self.nz, color, self.h2,
+            self.c[1 - color].data_ptr(), self.c[color].data_ptr(), self.r[color].data_ptr(), self.nbr.data_ptr(),
+            self.phi.stream()), "tm_gsrb_split_pass")
+
+    def sweep(self) -> None:
+        self.colour(0)
+        self.colour(1)
+
+    run = FusedGSRB.run
+
+    def finalize(self, plan=None) -> None:
+        from .multifab import fill_boundary
+
+        phi = self.phi
+        _native.check(_native.load().tm_gsrb_merge(
+            phi.layout.to_c(), phi.ptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
+            self.c[1].data_ptr(), phi.stream()), "tm_gsrb_merge")
+        fill_boundary(phi, self.geom, plan)

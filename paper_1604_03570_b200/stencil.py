@@ -213,25 +213,34 @@ def heat_amplification(params: HeatParams, geom: Geometry, modes=(1, 1, 1)) -> f
 
 
 def gsrb_solve(phi: MultiFab, rhs: MultiFab, geom: Geometry, sweeps: int, schedule=None, plan=None,
-               fused: bool | None = None, max_rows: int | None = None) -> MultiFab:
+               fused: bool | None = None, max_rows: int | None = None, split: bool | None = None) -> MultiFab:
     """``sweeps`` red-black sweeps (each: red, FillBoundary, black,
     FillBoundary -- BASELINE config 4).  With ``fused`` (default: whenever
     the layout allows) every colour pass is ONE launch that also scatters
-    the updated colour into the neighbours' halos (march.FusedGSRB); the
+    the updated colour into the neighbours' halos (march.FusedGSRB); with
+    ``split`` (default: whenever eligible) the solve runs on colour-split
+    storage, each pass reading only the other colour (march.SplitGSRB).  The
     result is bit-identical to the unfused loop and every ghost is filled
     on return."""
-    from .march import FusedGSRB, fusable
+    from .march import FusedGSRB, SplitGSRB, fusable, split_eligible
     from .multifab import comm_info
 
     _check_poisson(phi, rhs)
-    can = comm_info()[1] == 1 and fusable(phi, geom)
+    route_key = ("gsrb_route", geom, id(rhs), rhs.layout, comm_info()[1])
+    route = phi._plans.get(route_key)
+    if route is None:  # layout checks cost host time: once per (phi, rhs, geometry)
+        can_ = comm_info()[1] == 1 and fusable(phi, geom)
+        route = (can_, can_ and split_eligible(phi, rhs, geom))
+        phi._plans[route_key] = route
+    can, split_ok = route
     if fused and not can:
         raise ValueError("fused GSRB needs one rank and a uniform fully-covered box layout")
     if (can if fused is None else fused):
-        key = ("fused_gsrb", id(rhs), max_rows)
+        use_split = split_ok if split is None else split
+        key = ("fused_gsrb", id(rhs), max_rows, use_split)
         fg = phi._plans.get(key)
         if fg is None:
-            fg = FusedGSRB(phi, rhs, geom, max_rows)
+            fg = (SplitGSRB if use_split else FusedGSRB)(phi, rhs, geom, max_rows)
             phi._plans[key] = fg
         fg.prime(plan)
         fg.run(sweeps)

@@ -91,20 +91,21 @@ def gsrb_config(oracle: bool):
     plan = tm.build_fill_plan(phi, geom)
     sched = tm.build_schedule(phi, w.tile_size)
     tm.gsrb_solve(phi, rhs, geom, 2, sched, plan, fused=True)  # warm (plans, halo tables, graph)
+    tm.gsrb_solve(phi, rhs, geom, 2, sched, plan, fused=True, split=False)
     tm.gsrb_sweep(phi, rhs, geom, sched, plan)
     phi.fill(0.0)
     r0 = tm.residual_maxnorm(phi, rhs, geom, sched)
     res = {"config": "C4", "cells": w.cells, "sweeps": w.steps, "residual0": r0}
     finals = {}
-    for fused in (True, False):
+    for key, fused, split in (("fused", True, None), ("inplace", True, False), ("unfused", False, False)):
         phi.fill(0.0)
-        secs = ev_time(lambda: tm.gsrb_solve(phi, rhs, geom, w.steps, sched, plan, fused=fused))
-        key = "fused" if fused else "unfused"
+        secs = ev_time(lambda: tm.gsrb_solve(phi, rhs, geom, w.steps, sched, plan, fused=fused, split=split))
         res[key + "_rate"] = w.cells * w.steps / secs
         res[key + "_ms_per_sweep"] = secs / w.steps * 1e3
         res[key + "_residual"] = tm.residual_maxnorm(phi, rhs, geom, sched)
         finals[key] = phi.to_global()
-    res["fused_equals_unfused"] = bool(torch.equal(finals["fused"], finals["unfused"]))
+    res["fused_equals_unfused"] = bool(torch.equal(finals["fused"], finals["unfused"]) and
+                                       torch.equal(finals["inplace"], finals["unfused"]))
     r1 = res["fused_residual"]
     res["residual_decreased"] = r1 < r0
     if oracle:
