@@ -189,7 +189,21 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
         const tm_block c = a.cols[sg.col];
         const int nk = sg.k1 - sg.k0;
         const int yv0 = c.y0 - 1, zv0 = c.z0 - 1 + sg.k0;  // valid y of row 0, valid z of the first plane
-        const int32_t *nb = a.nbr + 6 * c.slot;
+        // neighbour slot deltas in registers (the scatter stores could alias a global table)
+        int64_t dn[6];
+        bool hn[6];
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+            const int32_t t = a.nbr[6 * c.slot + f];
+            hn[f] = t >= 0;
+            dn[f] = (int64_t)(t - c.slot) * C.slot;
+        }
+        dn[0] += nh;                        // x = 0 -> -x neighbour's entry nh
+        dn[1] -= nh;                        // x = nx-1 -> +x neighbour's entry -1
+        dn[2] += (int64_t)C.ny * C.row;     // row 0 -> -y neighbour's row ny
+        dn[3] -= (int64_t)C.ny * C.row;     // row ny-1 -> +y neighbour's row -1
+        dn[4] += (int64_t)C.nz * C.plane;   // plane 0 -> -z neighbour's plane nz
+        dn[5] -= (int64_t)C.nz * C.plane;   // plane nz-1 -> +z neighbour's plane -1
         const bool lane_on = lane * CPL < nh;
         const int ii = min(lane * CPL, nh - CPL);  // lane's first entry
         int rr[RPW];
@@ -252,30 +266,20 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
                     const int e_i = ii + j;
-                    if (o == 0 && e_i == 0 && nb[0] >= 0)  // x = 0 -> -x neighbour's x = nx (entry nh)
-                        d[j + nh - 0 + (int64_t)(nb[0] - c.slot) * C.slot] = out[i][j];
-                    if (o == 1 && e_i == nh - 1 && nb[1] >= 0)  // x = nx-1 -> +x neighbour's x = -1 (entry -1)
-                        d[j - nh + (int64_t)(nb[1] - c.slot) * C.slot] = out[i][j];
+                    if (o == 0 && e_i == 0 && hn[0]) d[j + dn[0]] = out[i][j];
+                    if (o == 1 && e_i == nh - 1 && hn[1]) d[j + dn[1]] = out[i][j];
                 }
-                if (yv == 0 && nb[2] >= 0) {  // row 0 -> -y neighbour's row ny
-                    double *q = d + (int64_t)(nb[2] - c.slot) * C.slot + (int64_t)C.ny * C.row;
+                const bool sy = (yv == 0 && hn[2]) || (yv == C.ny - 1 && hn[3]);
+                if (sy) {
+                    const int64_t dy = yv == 0 ? dn[2] : dn[3];
 #pragma unroll
-                    for (int j = 0; j < CPL; ++j) q[j] = out[i][j];
+                    for (int j = 0; j < CPL; ++j) d[j + dy] = out[i][j];
                 }
-                if (yv == C.ny - 1 && nb[3] >= 0) {  // row ny-1 -> +y neighbour's row -1
-                    double *q = d + (int64_t)(nb[3] - c.slot) * C.slot - (int64_t)C.ny * C.row;
+                const bool sz = (zv == 0 && hn[4]) || (zv == C.nz - 1 && hn[5]);
+                if (sz) {
+                    const int64_t dz = zv == 0 ? dn[4] : dn[5];
 #pragma unroll
-                    for (int j = 0; j < CPL; ++j) q[j] = out[i][j];
-                }
-                if (zv == 0 && nb[4] >= 0) {  // plane 0 -> -z neighbour's plane nz
-                    double *q = d + (int64_t)(nb[4] - c.slot) * C.slot + (int64_t)C.nz * C.plane;
-#pragma unroll
-                    for (int j = 0; j < CPL; ++j) q[j] = out[i][j];
-                }
-                if (zv == C.nz - 1 && nb[5] >= 0) {  // plane nz-1 -> +z neighbour's plane -1
-                    double *q = d + (int64_t)(nb[5] - c.slot) * C.slot - (int64_t)C.nz * C.plane;
-#pragma unroll
-                    for (int j = 0; j < CPL; ++j) q[j] = out[i][j];
+                    for (int j = 0; j < CPL; ++j) d[j + dz] = out[i][j];
                 }
             }
         }
