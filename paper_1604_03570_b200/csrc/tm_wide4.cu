@@ -40,7 +40,10 @@ struct W4Args {
     int32_t box_x, box_y, stage_elems;
 };
 
-template <int CPL, int NWARP>
+// PAIR: lane l owns the adjacent cells 2l, 2l+1 (widths 34..64): the x window of both
+// cells is five 16-B shared loads and every y neighbour pair one, instead of a
+// scalar load per neighbour per cell.
+template <int CPL, int NWARP, bool PAIR = false>
 __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     wide4_kernel(const __grid_constant__ CUtensorMap map, W4Args a) {
     using namespace tmk;
@@ -114,12 +117,13 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
         uint32_t coff[CPL];  // smem byte offset of cell j in a stage (rows past max_ny clamp; never stored)
 #pragma unroll
         for (int j = 0; j < CPL; ++j) {
-            const int x = lane + 32 * j;
-            on[j] = x < c.nx && r < c.ny;
+            const int x = PAIR ? min(2 * lane, bx - 2 * kR - 2) + j : lane + 32 * j;
+            on[j] = (PAIR ? 2 * lane + j : x) < c.nx && r < c.ny;
             coff[j] = (uint32_t)((min(r, max_ny - 1) + kR) * bx + min(x, bx - 2 * kR - 1) + kR) * 8u;
         }
         double *const orow = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)r * st.row;
-        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 + lane);
+        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 +
+                                   (PAIR ? 2 * lane : lane));
 
         // window w[m] = u at plane k-4+m of this lane's cells; prime with planes k0-4 .. k0+3
         double w[2 * kR + 1][CPL];
@@ -142,6 +146,39 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
             if (kk + 2 * kR >= nk + kR) release(qn);  // trailing halo plane: window use only
             const uint32_t sc = saddr(g + (uint32_t)kk + kR);  // centre plane k
             double out[CPL];
+            if constexpr (PAIR) {
+                const double cm[kR + 1] = {c0, c1, c2, c3, c4};
+                const uint32_t p0 = sc + coff[0];  // cell 2l; its x window starts 4 cells left
+                double v[2 * kR + 2];
+#pragma unroll
+                for (int q = 0; q < kR + 1; ++q) lds_f64x2(p0 - 8u * kR + 16u * q, v[2 * q], v[2 * q + 1]);
+                double sx[2], sy[2], sz[2];
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const double cu = rn_mul(c0, w[kR][j]);
+                    sx[j] = cu;
+                    sy[j] = cu;
+                    sz[j] = cu;
+                }
+#pragma unroll
+                for (int m = 1; m <= kR; ++m) {
+                    double ym0, ym1, yp0, yp1;
+                    lds_f64x2(p0 - ystep * m, ym0, ym1);
+                    lds_f64x2(p0 + ystep * m, yp0, yp1);
+                    sx[0] = rn_add(sx[0], rn_mul(cm[m], rn_add(v[kR - m], v[kR + m])));
+                    sx[1] = rn_add(sx[1], rn_mul(cm[m], rn_add(v[kR + 1 - m], v[kR + 1 + m])));
+                    sy[0] = rn_add(sy[0], rn_mul(cm[m], rn_add(ym0, yp0)));
+                    sy[1] = rn_add(sy[1], rn_mul(cm[m], rn_add(ym1, yp1)));
+#pragma unroll
+                    for (int j = 0; j < 2; ++j)
+                        sz[j] = rn_add(sz[j], rn_mul(cm[m], rn_add(w[kR - m][j], w[kR + m][j])));
+                }
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const double lap = rn_add(rn_add(rn_mul(sx[j], d0), rn_mul(sy[j], d1)), rn_mul(sz[j], d2));
+                    out[j] = rn_add(w[kR][j], rn_mul(dtD, lap));
+                }
+            } else
 #pragma unroll
             for (int j = 0; j < CPL; ++j) {
                 const uint32_t p0 = sc + coff[j];
@@ -166,9 +203,13 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
                 out[j] = rn_add(uc, rn_mul(dtD, lap));
             }
             release(g + (uint32_t)kk + kR);
+            if constexpr (PAIR) {
+                if (on[1]) *reinterpret_cast<double2 *>(orow + koff) = make_double2(out[0], out[1]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < CPL; ++j)
-                if (on[j]) orow[koff + 32 * j] = out[j];
+                for (int j = 0; j < CPL; ++j)
+                    if (on[j]) orow[koff + 32 * j] = out[j];
+            }
             koff += pstep;
 #pragma unroll
             for (int m = 0; m < 2 * kR; ++m)
@@ -179,9 +220,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     }
 }
 
-template <int CPL, int NWARP>
+template <int CPL, int NWARP, bool PAIR = false>
 int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = wide4_kernel<CPL, NWARP>;
+    auto kern = wide4_kernel<CPL, NWARP, PAIR>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -241,6 +282,7 @@ int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold
     cudaStream_t s = as_stream(stream);
     const int cpl = (p->max_nx + 31) / 32;
     if (cpl == 1) return launch_wide4_one<1, 16>(map, a, p->nctas, ncomp_sweep, smem, s);
+    if (cpl == 2 && p->even) return launch_wide4_one<2, 16, true>(map, a, p->nctas, ncomp_sweep, smem, s);
     if (cpl == 2) return launch_wide4_one<2, 16>(map, a, p->nctas, ncomp_sweep, smem, s);
     if (p->max_ny > 8) return fail(TM_ERR_INVALID, "tm_wide4_march: columns wider than 64 must be <= 8 rows");
     return launch_wide4_one<4, 8>(map, a, p->nctas, ncomp_sweep, smem, s);
