@@ -230,11 +230,15 @@ class FusedHalo2:
             heat_march2(new, old, params, max_rows=self.max_rows, nctas=self.nctas, nbr27=self.nbr)
 
 
-def face_neighbors(mf: MultiFab, geom: Geometry):
+REMOTE = -2  # face_neighbors entry: the neighbour lives on another rank
+
+
+def face_neighbors(mf: MultiFab, geom: Geometry, allow_remote: bool = False):
     """Per local slot, the slots of the 6 face neighbours (-x,+x,-y,+y,-z,+z),
     or None when the layout is not fusable: every face must be covered by
-    exactly one LOCAL box of identical extents (uniform chopped domains,
-    periodic or interior faces)."""
+    exactly one box of identical extents (uniform chopped domains, periodic
+    or interior faces) that is LOCAL -- or, with ``allow_remote``, on another
+    rank (entry ``REMOTE``: the kernels skip it, the halo exchange fills it)."""
     valids = [u.valid for u in mf.units]
     index = BoxIndex(valids)
     dom = geom.domain
@@ -259,12 +263,15 @@ def face_neighbors(mf: MultiFab, geom: Geometry):
                     return None
                 nb = hits[0]
                 if nb not in mf.slot_of:
-                    return None
+                    if not allow_remote:
+                        return None
+                    table[s, 2 * d + side] = REMOTE
+                    continue
                 table[s, 2 * d + side] = mf.slot_of[nb]
     return table
 
 
-def fusable(mf: MultiFab, geom: Geometry) -> bool:
+def fusable(mf: MultiFab, geom: Geometry, allow_remote: bool = False) -> bool:
     if not march_eligible(mf):
         return False
     ext = {mf.units[u].valid.extents for u in mf.local_units}
@@ -274,7 +281,7 @@ def fusable(mf: MultiFab, geom: Geometry) -> bool:
     L = mf.layout
     if ny % 2 or (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
         return False
-    return face_neighbors(mf, geom) is not None
+    return face_neighbors(mf, geom, allow_remote) is not None
 
 
 def neighbors27(mf: MultiFab, geom: Geometry):
@@ -357,14 +364,31 @@ def xh_init_plan(mf: MultiFab, table, nyv: int, nzv: int):
     return _native.CopyPlan(tags, mf.ncomp), (1, 2 * nyv, 2 * nyv * nzv)
 
 
+def xh_own_ghost_plan(mf: MultiFab, sides, nyv: int, nzv: int):
+    """Copy tags: the packed x halo of (slot, side) <- the slot's own ghost
+    column (x = -1 for side 0, x = nx for side 1), valid y and z, all
+    components -- valid after a FillBoundary / halo exchange."""
+    L = mf.layout
+    tags = np.zeros(len(sides), dtype=_native.COPY_TAG_DTYPE)
+    for t, (s, side) in enumerate(sides):
+        nx = mf.units[mf.local_units[s]].valid.extents[0]
+        src = s * L.slot + L.nghost * L.plane + L.nghost * L.row + (L.xoff - 1 if side == 0 else L.xoff + nx)
+        dst = ((s * mf.ncomp) * nzv * 2 + side) * nyv
+        tags[t] = (dst, src, 1, nyv, nzv, 0)
+    return _native.CopyPlan(tags, mf.ncomp), (1, 2 * nyv, 2 * nyv * nzv)
+
+
 class FusedHalo:
     """Packed x halos + neighbour table shared by an old/new MultiFab pair."""
 
     def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, max_rows: int | None = None,
-                 nctas: int | None = None):
+                 nctas: int | None = None, fill_plan=None):
         import torch
 
-        if not (fusable(a, geom) and a.same_layout(b)):
+        from .multifab import comm_info
+
+        multi = comm_info()[1] > 1
+        if not (fusable(a, geom, multi) and a.same_layout(b)):
             raise ValueError("layout is not eligible for the fused halo path")
         self.geom = geom
         L = a.layout
@@ -374,10 +398,20 @@ class FusedHalo:
         shape = (L.nslots * nc, self.nzv, 2, self.nyv)
         self.xh = {id(a): torch.zeros(shape, dtype=torch.float64, device=a.device),
                    id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
-        table = face_neighbors(a, geom)
+        table = face_neighbors(a, geom, multi)
         self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=a.device)
         self.plan = march_plan(a, True, max_rows, nctas)
-        self._init_plan = self._xh_init_plan(a, table)
+        # faces whose neighbour is on another rank: filled by the halo exchange after each
+        # step; x faces then copied from the ghost column into the packed x halo
+        remote_x = [(s, side) for s in range(table.shape[0]) for side in (0, 1) if table[s, side] == REMOTE]
+        self.remote = bool((table == REMOTE).any())
+        self.fill_plan = fill_plan
+        if self.remote:
+            every = [(s, side) for s in range(table.shape[0]) for side in (0, 1)]
+            self._init_plan, self.xh_side = xh_own_ghost_plan(a, every, self.nyv, self.nzv)
+            self._remote_x = xh_own_ghost_plan(a, remote_x, self.nyv, self.nzv)[0] if remote_x else None
+        else:
+            self._init_plan = self._xh_init_plan(a, table)
 
     def _xh_init_plan(self, mf: MultiFab, table) -> "_native.CopyPlan":
         plan, self.xh_side = xh_init_plan(mf, table, self.nyv, self.nzv)
@@ -403,6 +437,18 @@ class FusedHalo:
             self.plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
             self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
             old.stream()), "tm_heat_march(fused)")
+        if self.remote:  # faces shared with other ranks: NCCL exchange of the new field's boundary
+            from .fillplan import build_fill_plan
+            from .multifab import _device_fill
+
+            if self.fill_plan is None:
+                self.fill_plan = build_fill_plan(new, self.geom)
+            _, halo = _device_fill(new, self.fill_plan)
+            stream = new.stream()
+            halo.start(new, stream)
+            halo.finish(new, stream)
+            if self._remote_x is not None:
+                self._remote_x.run(self.xh[id(new)].data_ptr(), self.xh_side, new.ptr, new.layout.side(), stream)
 
 
 class FusedGSRB:

@@ -19,9 +19,10 @@ Two step implementations, bit-identical in the valid cells:
   regular FillBoundary at the end of ``advance``, so the MultiFab handed
   back has every ghost filled.
 
-Multi-rank runs (NCCL halo exchange) step eagerly with ``fused=False``: the
-interior tiles are swept while the halo messages are in flight
-(``stencil.overlapped_step``).
+Multi-rank runs step eagerly.  Fused: the march scatters into local
+neighbours and the faces shared with other ranks travel as one packed NCCL
+exchange of the new field right after it.  Unfused: the interior tiles are
+swept while the halo messages are in flight (``stencil.overlapped_step``).
 """
 
 from __future__ import annotations
@@ -52,11 +53,11 @@ class HeatRunner:
         self.zmerge = zmerge
         world = comm_info()[1]
         self.use_graph = (world == 1) if use_graph is None else (use_graph and world == 1)
-        can_fuse = world == 1 and march.fusable(mf, geom)
+        can_fuse = march.fusable(mf, geom, allow_remote=world > 1)
         if fused and not can_fuse:
-            raise ValueError("fused halo path needs one rank and a uniform fully-covered box layout")
+            raise ValueError("fused halo path needs a uniform fully-covered box layout")
         self.fused = can_fuse if fused is None else fused
-        self.fh = march.FusedHalo(self.a, self.b, geom, march_rows) if self.fused else None
+        self.fh = march.FusedHalo(self.a, self.b, geom, march_rows, fill_plan=self.plan) if self.fused else None
         self._graph = None
         self._primed = False
         self.steps_done = 0
@@ -68,6 +69,9 @@ class HeatRunner:
     @property
     def launches_per_step(self) -> int:
         if self.fused:
+            # multi-rank: march, pack, unpack (+ x-halo refresh when an x face is remote)
+            if self.fh.remote:
+                return 3 + (self.fh._remote_x is not None)
             return 1
         # multi-rank: pack, local copies, interior sweep, unpack, boundary sweep
         return 5 if self.a.dm.nranks > 1 else 2

@@ -2,8 +2,9 @@
 cuda:0 and exchange halos through torch.distributed (gloo, host-staged; the
 bench uses NCCL over NVLink with the same pack / send-recv / unpack code).
 No kernel waits on another process, so sharing the device is safe.  Checks
-the overlapped step (interior sweep while messages are in flight), the
-multi-rank checksum protocol and max/min against the single-rank oracle."""
+the overlapped step (interior sweep while messages are in flight), the fused
+march with its cross-rank face exchange, the multi-rank checksum protocol and
+max/min against the single-rank oracle."""
 
 import os
 import socket
@@ -24,7 +25,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, out):
+def worker(rank, world, port, out, fused):
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
@@ -42,8 +43,10 @@ def worker(rank, world, port, out):
         mf = tm.MultiFab(ba, w.ncomp, w.nghost)  # DistributionMapping over the gloo world
         mf.from_global(glob)
         p = tm.HeatParams.stable(1.0, geom.dx)
-        r = HeatRunner(mf, geom, p, w.tile_size)
-        assert not r.fused and not r.use_graph
+        r = HeatRunner(mf, geom, p, w.tile_size, fused=fused)
+        assert r.fused == fused and not r.use_graph
+        if fused:  # the 27 boxes split mid-layer: remote neighbours in x, y and z
+            assert r.fh.remote
         fin = r.advance(w.steps)
         got = fin.to_global().cpu().numpy()  # only this rank's boxes are non-zero
         c = p.coefficients()
@@ -63,10 +66,13 @@ def worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu_match_oracle():
+@pytest.mark.parametrize("fused", [False, True])
+def test_two_ranks_one_gpu_match_oracle(fused):
+    """fused=False: the overlapped unfused step; fused=True: the fused march
+    with the remote faces exchanged after each step."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(worker, args=(2, free_port(), out), nprocs=2, join=True)
+    mp.spawn(worker, args=(2, free_port(), out, fused), nprocs=2, join=True)
     for r in range(2):
         ok, sums_ok, max_ok, min_ok, n = out[r]
         assert ok, f"rank {r}: boxes differ from the oracle"
