@@ -89,6 +89,14 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
                                   dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
 
 
+def loop_heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatParams, workers: int = 1,
+                   scratch: dict | None = None) -> None:
+    """The reference's loop-level threading baseline (kernels.py:250-305) is a
+    CPU variant of the same arithmetic; on the device it is ``heat_step``
+    (same bits).  ``scratch`` is accepted and left empty."""
+    heat_step(mf_new, mf_old, geom, params, None, workers)
+
+
 def heat_sweep_plan(mf_new: MultiFab, mf_old: MultiFab, params: HeatParams, plan) -> None:
     """Kernel A over an explicit block table (e.g. the interior or boundary
     half of an overlapped step).  No checks: internal helper."""
