@@ -235,3 +235,23 @@ def test_split_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
     tm.gsrb_solve(phi, rhs, geom, 2, fused=True, split=True, max_rows=rows)
     tm.gsrb_solve(phi2, rhs, geom, 2, fused=True, split=False)
     assert np.array_equal(phi.to_global().cpu().numpy(), phi2.to_global().cpu().numpy())
+
+
+def test_c4_full_size_split_inplace_unfused_agree(tm):
+    """BASELINE config 4 at full size (256^3, 64 boxes, 50 sweeps): the
+    colour-split, in-place fused and unfused solves give the same bits and the
+    residual decreases (size-independent properties; the oracle check runs at
+    reduced sizes above)."""
+    w = tm.CONFIGS["C4"]
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    rhs = tm.MultiFab(ba, 1, 0)
+    rhs.from_global(tm.make_init(w))
+    out = []
+    for fused, split in ((True, True), (True, False), (False, False)):
+        phi = tm.MultiFab(ba, 1, 1)
+        r0 = tm.residual_maxnorm(phi, rhs, geom) if not out else None
+        tm.gsrb_solve(phi, rhs, geom, w.steps, fused=fused, split=split)
+        out.append((phi.to_global().cpu().numpy(), tm.residual_maxnorm(phi, rhs, geom), r0))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][0], out[2][0])
+    assert out[0][1] == out[1][1] == out[2][1] < out[0][2]
