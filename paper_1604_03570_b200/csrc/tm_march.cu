@@ -172,6 +172,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
             orow[i] = obase + (int64_t)r * st.row;
             roff[i] = (uint32_t)((min(r, max_ny) + 1) * bx + xi + xsh) * 8u;
         }
+        // the row after this warp's last row (its y+1 neighbours): clamped to the stage's last
+        // row for warps whose rows all lie past the column (values never stored)
+        const uint32_t ypo = (uint32_t)((min(warp * RPW + RPW - 1, max_ny - 1) + 2) * bx + xi + xsh) * 8u;
         uint32_t xlo[RPW], xro[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
@@ -255,10 +258,10 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2) {
                         lds_f64x2(sc + roff[0] - ystep + 8u * j, ym[j], ym[j + 1]);
-                        lds_f64x2(sc + roff[RPW - 1] + ystep + 8u * j, yp[j], yp[j + 1]);
+                        lds_f64x2(sc + ypo + 8u * j, yp[j], yp[j + 1]);
                     } else {
                         ym[j] = lds_f64(sc + roff[0] - ystep + 8u * j);
-                        yp[j] = lds_f64(sc + roff[RPW - 1] + ystep + 8u * j);
+                        yp[j] = lds_f64(sc + ypo + 8u * j);
                     }
                 }
 #pragma unroll
@@ -464,6 +467,8 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
             xro[i] = (xc + CPL == c.nx) ? (uint32_t)(a.xh_off + ny_box + rc) * 8u : roff[i] + (uint32_t)CPL * 8u;
             rof[i] = (uint32_t)(ga.rhs_off + min(r, ny_box - 1) * bx + xc) * 8u;
         }
+        // y+1 row of this warp's last row, clamped inside the stage (see march_kernel)
+        const uint32_t ypo = (uint32_t)((min(warp * RPW + RPW - 1, ny_box - 1) + 2) * bx + xc) * 8u;
         // colour of this lane's cell 0 in row 0 at plane k0, flipped per row and per plane
         const int par0 = (c.parity + xc + warp * RPW + sg.k0 + ga.color) & 1;
         // scatter targets (see march_kernel)
@@ -538,7 +543,7 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
                 if constexpr (CPL == 1) {
                     const double xl = lds_f64(sc + xlo[i]), xr = lds_f64(sc + xro[i]);
                     const double ym = i > 0 ? uc[i - 1][0] : lds_f64(sc + roff[0] - ystep);
-                    const double yp = i < RPW - 1 ? uc[i + 1][0] : lds_f64(sc + roff[RPW - 1] + ystep);
+                    const double yp = i < RPW - 1 ? uc[i + 1][0] : lds_f64(sc + ypo);
                     const double rh = lds_f64(sc + rof[i]);
                     double sum = rn_add(rn_add(rn_add(rn_add(rn_add(xl, xr), ym), yp), um[i][0]), un[i][0]);
                     const double upd = __ddiv_rn(rn_add(sum, rn_mul(h2, rh)), 6.0);
@@ -554,7 +559,7 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
                         const double ym = i > 0 ? (p ? uc[i - 1][j0 + 1] : uc[i - 1][j0])
                                                 : lds_f64(sc + roff[0] - ystep + jb);
                         const double yp = i < RPW - 1 ? (p ? uc[i + 1][j0 + 1] : uc[i + 1][j0])
-                                                      : lds_f64(sc + roff[RPW - 1] + ystep + jb);
+                                                      : lds_f64(sc + ypo + jb);
                         const double zm = p ? um[i][j0 + 1] : um[i][j0];
                         const double zp = p ? un[i][j0 + 1] : un[i][j0];
                         const double rh = lds_f64(sc + rof[i] + jb);
@@ -634,6 +639,7 @@ int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArg
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
         if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
         if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
         if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
         return launch_march_one<2, 16, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);

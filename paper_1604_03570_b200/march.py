@@ -57,7 +57,7 @@ def warps_for(nx: int, rows: int) -> int:
     """Consumer warps of the march kernel instance (mirrors launch_march)."""
     if nx > 64:
         return 8 if rows <= 8 else 16
-    return 4 if rows <= 8 else (8 if rows <= 16 else 16)
+    return 4 if rows <= 8 else (7 if rows <= 14 else (8 if rows <= 16 else 16))
 
 
 def max_rows_for(nx: int, packed: bool) -> int:

@@ -63,6 +63,8 @@ def test_heat_march_std_matches_oracle(tm, cfg, n, mgs, steps, rows, nctas):
     ("C2", 96, 32, 5, 8, False),
     ("C3", 128, 64, 3, 16, True),
     ("C5", 64, 32, 4, None, True),
+    ("C2", 128, 64, 3, 12, True),   # 7 warps x 2 rows over 10/12-row columns: rows past the column
+    ("C2", 128, 64, 2, 10, False),  # (8 warps x 2 rows over 10-row columns)
 ])
 def test_fused_runner_matches_oracle(tm, cfg, n, mgs, steps, rows, graph):
     import torch
@@ -112,7 +114,7 @@ def test_fusable_rules(tm):
 
 
 @pytest.mark.parametrize("n,mgs,sweeps,rows", [(64, 32, 5, None), (64, 32, 4, 8), (32, 16, 6, None),
-                                               (128, 64, 3, None)])
+                                               (128, 64, 3, None), (128, 64, 2, 12)])
 def test_fused_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
     w = tm.CONFIGS["C4"].scaled(n, mgs, sweeps)
     rhs_g = tm.make_init(w)
@@ -121,14 +123,14 @@ def test_fused_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
     phi = tm.MultiFab(ba, 1, 1)
     rhs = tm.MultiFab(ba, 1, 0)
     rhs.from_global(rhs_g)
-    tm.gsrb_solve(phi, rhs, geom, sweeps, fused=True, max_rows=rows)
+    tm.gsrb_solve(phi, rhs, geom, sweeps, fused=True, split=False, max_rows=rows)  # in-place kernel
     ref_phi, ref_res = orc.gsrb_periodic(np.zeros((n,) * 3), rhs_g[0], sweeps, w.dx * w.dx)
     assert np.array_equal(phi.to_global().cpu().numpy()[0], ref_phi)
     assert tm.residual_maxnorm(phi, rhs, geom) == ref_res
     # a second solve continues from the current state, fused == unfused
     phi2 = tm.MultiFab(ba, 1, 1)
     phi2.data.copy_(phi.data)
-    tm.gsrb_solve(phi, rhs, geom, 2, fused=True, max_rows=rows)
+    tm.gsrb_solve(phi, rhs, geom, 2, fused=True, split=False, max_rows=rows)
     tm.gsrb_solve(phi2, rhs, geom, 2, fused=False)
     assert np.array_equal(phi.to_global().cpu().numpy(), phi2.to_global().cpu().numpy())
 

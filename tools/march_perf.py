@@ -36,7 +36,7 @@ def main():
             pl = march.march_plan(a, False, rows, nctas)
             print(f"{cfg} march-std rows={rows} nctas={pl.nctas} cols={pl.ncolumns}: {ms * 1e3:.1f} us "
                   f"{16 * cells / ms / 1e6:.0f} GB/s alg ({cells / ms / 1e6:.1f} G cell/s)")
-    for rows in (None, 32, 16, 8):
+    for rows in (None, 32, 16, 14, 12, 8):
         for mult in ((None,) if "--fused-only" in sys.argv else (None, 2, 3, 4)):
             nctas = None if mult is None else nsm * mult
             try:
