@@ -114,7 +114,7 @@ def test_fusable_rules(tm):
 
 
 @pytest.mark.parametrize("n,mgs,sweeps,rows", [(64, 32, 5, None), (64, 32, 4, 8), (32, 16, 6, None),
-                                               (128, 64, 3, None), (128, 64, 2, 12)])
+                                               (128, 64, 3, None), (128, 64, 2, 12), (128, 128, 2, None)])
 def test_fused_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
     w = tm.CONFIGS["C4"].scaled(n, mgs, sweeps)
     rhs_g = tm.make_init(w)
@@ -211,7 +211,8 @@ def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas, rows, pa
 
 
 @pytest.mark.parametrize("n,mgs,sweeps,rows", [(64, 32, 5, None), (64, 32, 4, 8), (32, 16, 6, None),
-                                               (128, 64, 3, None), (48, 24, 3, 8)])
+                                               (128, 64, 3, None), (48, 24, 3, 8), (128, 128, 2, None),
+                                               (64, 64, 2, 12)])
 def test_split_gsrb_matches_oracle(tm, n, mgs, sweeps, rows):
     """Colour-split GSRB: phi and residual identical to the oracle and to the
     in-place fused path."""
