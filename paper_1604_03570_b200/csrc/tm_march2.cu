@@ -210,6 +210,14 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP <= 8 ? 2 : 1)
             }
         }
         const int zv0 = c.z0 - g_ng + sg.k0;  // valid z of the first output plane
+        // the y-face target of this row (rows within two layers of a y face), every plane
+        bool vyf = false;
+        int64_t dyf = 0;
+        if (SCAT && oyv != 0) {
+            const int T = nb[13 + 3 * oyv];
+            vyf = T >= 0;
+            dyf = (int64_t)(T - c.slot) * st.slot - (int64_t)oyv * a.nyb * st.row;
+        }
         // x halos: the lane holding cells 0,1 (nx-2, nx-1) feeds side 1 (side 0) of the -x (+x)
         // box; pointers for the face target and the (x, y) edge target follow the planes
         const bool x_role = PACKED && a.xh_new && (xi < 2 || xi + CPL > a.nxb - 2) && lane * CPL < c.nx;
@@ -380,59 +388,50 @@ __global__ void __launch_bounds__(NWARP * 32, NWARP <= 8 ? 2 : 1)
             if (on) {
                 put(0);
                 if (SCAT && (HALO == 2 || a.xh_new)) {
-                    const int zv = zv0 + j - 2;
-                    int ozv = 0, zlay = 3;
-                    if (zv < 2) {
-                        ozv = -1;
-                        zlay = zv + 1;
-                    } else if (zv >= a.nzb - 2) {
-                        ozv = 1;
-                        zlay = a.nzb - zv;
-                    }
-                    // x halos of the -x / +x boxes: faces two deep, (x, y) and (x, z) edges one deep
-                    if (x_role) {
-                        auto xput = [&](double *q) {
-                            if constexpr (CPL >= 2)
-                                *reinterpret_cast<double2 *>(q) = make_double2(out[0], out[1]);
-                            else
-                                *q = out[0];
-                        };
+                    // every plane: x faces (+ this row's (x, y) edge) and this row's y face
+                    auto xput = [&](double *q) {
+                        if constexpr (CPL >= 2)
+                            *reinterpret_cast<double2 *>(q) = make_double2(out[0], out[1]);
+                        else
+                            *q = out[0];
+                    };
+                    if (HALO == 1) {
                         if (xq0) xput(xq0);
                         if (xq1) xput(xq1);
-                        if (ozv != 0 && zlay == 1) {  // two planes per column
-                            const int T2 = nb[(xside ? 12 : 14) + 9 * ozv];
-                            if (T2 >= 0) xput(xh_ptr(T2, 0, ozv, zv));
-                        }
-                    }
-                    if (HALO == 2) {
+                    } else {
                         if (vl0) put(dl0);
                         if (vr0) put(dr0);
                         if (vl1) put(dl1);
                         if (vr1) put(dr1);
-                        if (ozv != 0 && zlay == 1 && (cl || cr)) {  // (x, z) edges: two planes per column
-                            const int T2 = nb[(cl ? 12 : 14) + 9 * ozv];
-                            if (T2 >= 0)
-                                put((int64_t)(T2 - c.slot) * st.slot - (int64_t)ozv * a.nzb * st.plane +
-                                    (cl ? a.nxb : -a.nxb));
-                            if (cl && cr) {  // narrow boxes: the lane feeds both sides
-                                const int T3 = nb[14 + 9 * ozv];
-                                if (T3 >= 0)
-                                    put((int64_t)(T3 - c.slot) * st.slot - (int64_t)ozv * a.nzb * st.plane - a.nxb);
-                            }
-                        }
                     }
-                    // y / z ghost rows of the neighbours: faces two deep, the (y, z) edge one deep
-                    if (oyv != 0 || ozv != 0) {  // warp-uniform: boundary rows / planes only
-#pragma unroll
-                        for (int t = 1; t < 4; ++t) {
-                            if ((t & 1) && oyv == 0) continue;
-                            if ((t & 2) && ozv == 0) continue;
-                            const int oy = (t & 1) ? oyv : 0, oz = (t & 2) ? ozv : 0;
-                            if ((oy ? ylay : 0) + (oz ? zlay : 0) > 2) continue;
-                            const int T = nb[13 + 3 * oy + 9 * oz];
-                            if (T >= 0)
-                                put((int64_t)(T - c.slot) * st.slot - (int64_t)oz * a.nzb * st.plane -
-                                    (int64_t)oy * a.nyb * st.row);
+                    if (vyf) put(dyf);
+                    // the two planes next to each z face (warp-uniform, rare): z faces two deep,
+                    // (y, z) and (x, z) edges one deep
+                    const int zv = zv0 + j - 2;
+                    if (zv < 2 || zv >= a.nzb - 2) {
+                        const int ozv = zv < 2 ? -1 : 1, zlay = zv < 2 ? zv + 1 : a.nzb - zv;
+                        const int64_t dz = -(int64_t)ozv * a.nzb * st.plane;
+                        const int Tz = nb[13 + 9 * ozv];
+                        if (Tz >= 0) put((int64_t)(Tz - c.slot) * st.slot + dz);
+                        if (zlay == 1) {
+                            if (oyv != 0 && ylay == 1) {
+                                const int Tyz = nb[13 + 3 * oyv + 9 * ozv];
+                                if (Tyz >= 0) put((int64_t)(Tyz - c.slot) * st.slot + dz - (int64_t)oyv * a.nyb * st.row);
+                            }
+                            if (HALO == 1 && x_role) {
+                                const int T2 = nb[(xside ? 12 : 14) + 9 * ozv];
+                                if (T2 >= 0) xput(xh_ptr(T2, 0, ozv, zv));
+                            }
+                            if (HALO == 2) {
+                                if (cl) {
+                                    const int T2 = nb[12 + 9 * ozv];
+                                    if (T2 >= 0) put((int64_t)(T2 - c.slot) * st.slot + dz + a.nxb);
+                                }
+                                if (cr) {
+                                    const int T3 = nb[14 + 9 * ozv];
+                                    if (T3 >= 0) put((int64_t)(T3 - c.slot) * st.slot + dz - a.nxb);
+                                }
+                            }
                         }
                     }
                 }
