@@ -397,6 +397,7 @@ def run_ours(args, w):
         if cpu is not None:
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
+    runner.close()  # before the process group goes: a live graph may hold NCCL work
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

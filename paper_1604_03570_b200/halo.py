@@ -11,9 +11,13 @@ exchange:
   source unit a owns and whose destination unit b owns, each tag's cells
   packed x-fastest then y, z, component (``tm_side`` "packed" format);
 * rank a packs all its outgoing messages with one copy-kernel launch into
-  one send buffer, the messages go out as one grouped NCCL send/recv
-  (``torch.distributed.batch_isend_irecv``), and rank b unpacks all its
-  incoming messages with one launch straight into ghost cells.
+  one send buffer (messages in ascending peer order), every message of the
+  exchange travels in ONE ``torch.distributed.all_to_all_single`` call with
+  per-peer split sizes (NCCL: one grouped send/recv; zero-sized splits for
+  ranks that are not neighbours), and rank b unpacks all its incoming
+  messages with one launch straight into ghost cells.  One host call per
+  exchange keeps the issue cost low, and the collective is capturable in a
+  CUDA graph (``runner.HeatRunner`` replays multi-rank steps).
 
 Intra-rank tags never touch a buffer: they are the local copy kernel.
 """
@@ -65,6 +69,17 @@ def message_layout(tags, groups, ncomp: int):
     return rows, spans, off
 
 
+def split_sizes(spans, world: int) -> list:
+    """Per-rank element counts of a message buffer for
+    ``all_to_all_single``: spans' counts at their peers, 0 elsewhere (self
+    included).  Valid because ``message_layout`` orders messages by
+    ascending peer."""
+    sizes = [0] * world
+    for peer, _, n in spans:
+        sizes[peer] = n
+    return sizes
+
+
 class HaloExchange:
     """Pack / grouped send-recv / unpack for one (MultiFab layout, plan)."""
 
@@ -108,38 +123,38 @@ class HaloExchange:
         self.recvbuf = torch.empty(max(nrecv, 1), dtype=torch.float64, device=mf.device)
         self.bytes_sent = nsend * 8
         self.bytes_recv = nrecv * 8
-        self._reqs = None
+        self.nsend, self.nrecv = nsend, nrecv
+        self.send_splits = split_sizes(self.send_spans, mf.dm.nranks)
+        self.recv_splits = split_sizes(self.recv_spans, mf.dm.nranks)
+        self._work = None
+        self._host = None
 
     def start(self, mf, stream: int) -> None:
         """Pack every outgoing message of ``mf`` (one launch) and post the
-        grouped sends/receives.  NCCL orders them after the pack on the
-        current stream; ``finish`` makes the stream wait for the receives.
-        The exchange object is shared by every MultiFab of the same layout
-        (e.g. both buffers of a double-buffered pair), so the field is
-        passed per call."""
+        exchange (one all-to-all with per-peer splits).  NCCL orders it after
+        the pack on the current stream; ``finish`` makes the stream wait for
+        it and unpacks.  The exchange object is shared by every MultiFab of
+        the same layout (e.g. both buffers of a double-buffered pair), so the
+        field is passed per call."""
         import torch
         import torch.distributed as dist
 
-        packed = (0, 0, 0)
-        self.pack.run(self.sendbuf.data_ptr(), packed, mf.ptr, mf.layout.side(), stream)
-        self._host = dist.get_backend() == "gloo"
+        self.pack.run(self.sendbuf.data_ptr(), (0, 0, 0), mf.ptr, mf.layout.side(), stream)
+        if self._host is None:
+            self._host = dist.get_backend() == "gloo"
         if self._host:  # CPU transport (tests): stage through host memory
             torch.cuda.current_stream(self.device).synchronize()
-            sbuf = self.sendbuf.cpu()
-            self._hrecv = torch.empty(self.recvbuf.shape, dtype=torch.float64)
+            sbuf = self.sendbuf[:self.nsend].cpu()
+            self._hrecv = torch.empty(self.nrecv, dtype=torch.float64)
         else:
-            sbuf, self._hrecv = self.sendbuf, self.recvbuf
-        ops = []
-        for peer, off, n in self.send_spans:
-            ops.append(dist.P2POp(dist.isend, sbuf[off:off + n], peer))
-        for peer, off, n in self.recv_spans:
-            ops.append(dist.P2POp(dist.irecv, self._hrecv[off:off + n], peer))
-        self._reqs = dist.batch_isend_irecv(ops) if ops else []
+            sbuf, self._hrecv = self.sendbuf[:self.nsend], self.recvbuf[:self.nrecv]
+        self._work = dist.all_to_all_single(self._hrecv, sbuf, self.recv_splits, self.send_splits,
+                                            async_op=True)
 
     def finish(self, mf, stream: int) -> None:
-        for r in self._reqs or []:
-            r.wait()
-        self._reqs = None
+        if self._work is not None:
+            self._work.wait()
+        self._work = None
         if self._host:
-            self.recvbuf.copy_(self._hrecv)
+            self.recvbuf[:self.nrecv].copy_(self._hrecv)
         self.unpack.run(mf.ptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)

@@ -404,7 +404,9 @@ class FusedHalo:
         # faces whose neighbour is on another rank: filled by the halo exchange after each
         # step; x faces then copied from the ghost column into the packed x halo
         remote_x = [(s, side) for s in range(table.shape[0]) for side in (0, 1) if table[s, side] == REMOTE]
-        self.remote = bool((table == REMOTE).any())
+        # every rank joins the exchange (one collective per step), even one
+        # whose faces all happen to be local
+        self.remote = multi
         self.fill_plan = fill_plan
         if self.remote:
             every = [(s, side) for s in range(table.shape[0]) for side in (0, 1)]

@@ -19,13 +19,19 @@ Two step implementations, bit-identical in the valid cells:
   regular FillBoundary at the end of ``advance``, so the MultiFab handed
   back has every ghost filled.
 
-Multi-rank runs step eagerly.  Fused: the march scatters into local
-neighbours and the faces shared with other ranks travel as one packed NCCL
-exchange of the new field right after it.  Unfused: the interior tiles are
-swept while the halo messages are in flight (``stencil.overlapped_step``).
+Multi-rank: fused, the march scatters into local neighbours and the faces
+shared with other ranks travel as one packed all-to-all (NCCL) of the new
+field right after it; unfused, the interior tiles are swept while the halo
+messages are in flight (``stencil.overlapped_step``).  Over NCCL the step
+pair -- kernels and collectives -- is captured into the graph too, so a step
+costs no Python; the first captured pair is checked bit for bit against two
+eager steps on every rank (all-reduced verdict), and the runner falls back to
+eager steps if any rank disagrees.  ``TM_MULTI_GRAPH=0`` forces eager steps.
 """
 
 from __future__ import annotations
+
+import os
 
 from .boxarray import Geometry
 from .fillplan import FillPlan, build_fill_plan
@@ -52,7 +58,9 @@ class HeatRunner:
         self.schedule = schedule
         self.zmerge = zmerge
         world = comm_info()[1]
-        self.use_graph = (world == 1) if use_graph is None else (use_graph and world == 1)
+        graphable = world == 1 or _nccl_world()
+        self.use_graph = graphable if use_graph is None else (use_graph and graphable)
+        self._check_graph = world > 1
         can_fuse = march.fusable(mf, geom, allow_remote=world > 1)
         if fused and not can_fuse:
             raise ValueError("fused halo path needs a uniform fully-covered box layout")
@@ -81,6 +89,16 @@ class HeatRunner:
         self.steps_done = 0
         self._primed = False
 
+    def close(self) -> None:
+        """Release the captured graph.  Multi-rank: call before
+        ``destroy_process_group`` -- a live graph holding NCCL work blocks the
+        communicator's teardown."""
+        import torch
+
+        if self._graph is not None:
+            torch.cuda.synchronize()
+            self._graph = None
+
     def _step(self, old: MultiFab, new: MultiFab) -> None:
         if self.fused:  # b -> a steps walk backwards: they start where a -> b ended (L2)
             self.fh.step(new, old, self.params, reverse=old is self.b)
@@ -106,6 +124,33 @@ class HeatRunner:
                 self._step(self.b, self.a)
         torch.cuda.current_stream().wait_stream(s)
         self._graph = g
+        if self._check_graph:
+            self._verify_capture()
+
+    def _verify_capture(self) -> None:
+        """Multi-rank: replay the captured pair once and redo the same two
+        steps eagerly from the same state; keep the graph only if every rank
+        got identical bytes.  Leaves the state two steps ahead (eager)."""
+        import torch
+        import torch.distributed as dist
+
+        a = self.a
+        saved = [a.data.clone()]
+        if self.fused:
+            saved.append(self.fh.xh[id(a)].clone())
+        self._graph.replay()
+        got = a.data.clone()
+        a.data.copy_(saved[0])
+        if self.fused:
+            self.fh.xh[id(a)].copy_(saved[1])
+        self._step(self.a, self.b)
+        self._step(self.b, self.a)
+        same = torch.equal(got.view(torch.int64), a.data.view(torch.int64))
+        flag = torch.tensor([1 if same else 0], dtype=torch.int32, device=a.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) != 1:
+            self._graph = None
+            self.use_graph = False
 
     def advance(self, n: int, finalize: bool = True) -> MultiFab:
         """Advance ``n`` steps; returns the MultiFab holding the state (all
@@ -119,11 +164,13 @@ class HeatRunner:
                 self._step(self.b, self.a)
                 self.steps_done += 1
                 k += 1
-            if self.steps_done % 2 == 0 and n - k >= 2:
-                if self._graph is None:
-                    self._capture()  # runs two real steps
-                    self.steps_done += 2
-                    k += 2
+            # capturing runs two real steps, four when the capture is verified
+            need = 4 if self._check_graph else 2
+            if self.steps_done % 2 == 0 and self._graph is None and n - k >= need:
+                self._capture()
+                self.steps_done += need
+                k += need
+            if self.steps_done % 2 == 0 and self._graph is not None:
                 while n - k >= 2:
                     self._graph.replay()
                     self.steps_done += 2
@@ -136,3 +183,15 @@ class HeatRunner:
         if self.fused and finalize:
             fill_boundary(self.current, self.geom, self.plan)
         return self.current
+
+
+def _nccl_world() -> bool:
+    """Multi-rank steps may be graph-captured: NCCL collectives are."""
+    if os.environ.get("TM_MULTI_GRAPH", "1") == "0":
+        return False
+    try:
+        import torch.distributed as dist
+
+        return dist.is_initialized() and dist.get_backend() == "nccl"
+    except (ImportError, RuntimeError):  # pragma: no cover
+        return False

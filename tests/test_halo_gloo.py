@@ -4,7 +4,8 @@ Each rank owns the boxes DistributionMapping assigns it, derives its local /
 send / receive tag lists and packed message layouts from the GLOBAL plan
 (``halo.exchange_lists`` + ``halo.message_layout`` -- the same functions the
 GPU HaloExchange uses), packs its outgoing tags with numpy, exchanges the
-messages with ``batch_isend_irecv`` and unpacks.  The ghosts of every box a
+messages with one ``all_to_all_single`` (per-peer split sizes, as the
+device HaloExchange does) and unpacks.  The ghosts of every box a
 rank owns must equal the single-process oracle FillBoundary bit for bit.
 Also checks the multi-rank checksum protocol (partials all-reduced, then
 summed in grid order) against the serial reference sum.
@@ -22,7 +23,7 @@ import torch.multiprocessing as mp
 from oracle import oracle as orc
 from paper_1604_03570_b200 import Box, BoxArray, DistributionMapping, Geometry
 from paper_1604_03570_b200.fillplan import build_fill_plan_units
-from paper_1604_03570_b200.halo import exchange_lists, message_layout
+from paper_1604_03570_b200.halo import exchange_lists, message_layout, split_sizes
 
 NC, NG = 2, 2
 
@@ -88,11 +89,9 @@ def worker(rank, world, port, out):
         srows, sspans, stot = message_layout(plan.tags, sends, NC)
         rrows, rspans, rtot = message_layout(plan.tags, recvs, NC)
         sendbuf = torch.from_numpy(pack(h, plan.tags, srows, stot))
-        recvbuf = torch.empty(max(rtot, 1), dtype=torch.float64)
-        ops = [dist.P2POp(dist.isend, sendbuf[o:o + n], p) for p, o, n in sspans]
-        ops += [dist.P2POp(dist.irecv, recvbuf[o:o + n], p) for p, o, n in rspans]
-        for r in dist.batch_isend_irecv(ops) if ops else []:
-            r.wait()
+        recvbuf = torch.empty(rtot, dtype=torch.float64)
+        assert [o for _, o, _ in sspans] == sorted(o for _, o, _ in sspans)  # ascending peers
+        dist.all_to_all_single(recvbuf, sendbuf, split_sizes(rspans, world), split_sizes(sspans, world))
         unpack(h, plan.tags, rrows, recvbuf.numpy())
         ref = orc.HostMF(valids, NC, NG, fill=np.nan)
         ref.from_global(glob)
