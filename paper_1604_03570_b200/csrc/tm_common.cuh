@@ -71,6 +71,9 @@ __device__ __forceinline__ void fence_proxy_async_shared() {
 __device__ __forceinline__ void named_barrier_sync(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_barrier_arrive(int id, int nthreads) {
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 // 4-D tiled TMA store smem -> global (bulk-group completion)
 __device__ __forceinline__ void tma_store_plane(const CUtensorMap *map, uint32_t src, int x, int y, int z, int w) {
     asm volatile(

@@ -376,6 +376,7 @@ struct tm_sweep_plan {
     tm_block *d_blocks = nullptr;
     int max_nx = 0, max_ny = 0, max_seg = 0, cfg = 0;
     int vec = 0;  // vectorised heat kernel config, 0 = scalar kernel
+    int64_t max_cells = 0;  // largest block
     // small cache of encoded tensor maps keyed by (base pointer, layout)
     struct MapEntry {
         const double *base;
@@ -445,6 +446,7 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
     if (nblocks < 0 || (nblocks > 0 && !blocks)) return fail(TM_ERR_INVALID, "tm_sweep_plan_create: bad arguments");
     if (nblocks > (int64_t)INT32_MAX) return fail(TM_ERR_INVALID, "tm_sweep_plan_create: too many blocks");
     int mx = 1, my = 1, maxseg = 1;
+    int64_t maxcells = 0;
     bool even2 = true, even4 = true;
     for (int64_t b = 0; b < nblocks; ++b) {
         const tm_block &k = blocks[b];
@@ -452,6 +454,7 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
             return fail(TM_ERR_INVALID, "tm_sweep_plan_create: malformed block " + std::to_string(b));
         mx = std::max(mx, k.nx);
         my = std::max(my, k.ny);
+        maxcells = std::max(maxcells, (int64_t)k.nx * k.ny * k.nz);
         maxseg = std::max(maxseg, k.ny * ((k.nx + 31) / 32));
         even2 = even2 && (k.x0 % 2 == 0) && (k.nx % 2 == 0);
         even4 = even4 && (k.x0 % 2 == 0) && (k.nx % 4 == 0);
@@ -461,6 +464,7 @@ int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan 
     p->max_nx = mx;
     p->max_ny = my;
     p->max_seg = maxseg;
+    p->max_cells = maxcells;
     const int rows_cfg = my <= 8 ? 0 : my <= 16 ? 1 : my <= 32 ? 2 : my <= 64 ? 3 : -1;
     if (rows_cfg >= 0 && even2 && mx <= 64) p->vec = 1 + rows_cfg;
     else if (rows_cfg >= 0 && even4 && mx <= 128) p->vec = 5 + rows_cfg;
@@ -563,3 +567,5 @@ extern "C" int tm_internal_plan_blocks(const tm_sweep_plan *p, const tm_block **
     *n = p->nblocks;
     return TM_OK;
 }
+
+extern "C" int64_t tm_internal_plan_max_cells(const tm_sweep_plan *p) { return p->max_cells; }
