@@ -204,6 +204,18 @@ int tm_gsrb_split_pass(tm_march_plan *plan, int32_t nslots, int32_t nx, int32_t 
 int tm_wide4_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                    int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
                    double dtD, void *stream);
+/* Same step with FillBoundary fused into its epilogue (no reference
+ * counterpart: replaces the fill_boundary + wide4_step pair of the
+ * reference's step loop, level.py:297-323 + kernels.py:218-247, for uniform
+ * fully-covered box layouts): every cell within 4 of a box face is also
+ * written into the face neighbour's ghost layers of unew, so the next step's
+ * x/y/z face ghosts are filled on return (edge/corner ghosts are not: the
+ * stencil never reads them).  d_nbr = device int32[nslots][6] face neighbours
+ * (-x,+x,-y,+y,-z,+z; local slot, < 0: none); box_extents = host int32[3],
+ * the uniform box size (each >= 8). */
+int tm_wide4_march_fused(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                         int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                         double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream);
 
 /* ---- reductions (one block per unit, blocks in grid order) --------------- */
 /* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =

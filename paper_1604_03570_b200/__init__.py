@@ -39,6 +39,7 @@ from .stencil import (
 )
 from .wide4 import (
     StencilCoeffs8,
+    Wide4Runner,
     derive_coeffs8,
     loop_wide4_step,
     wide4_amplification,
@@ -57,7 +58,8 @@ __all__ = [
     "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
     "loop_heat_step",
     "residual_maxnorm",
-    "StencilCoeffs8", "derive_coeffs8", "loop_wide4_step", "wide4_amplification", "wide4_stable_dt", "wide4_step",
+    "StencilCoeffs8", "Wide4Runner", "derive_coeffs8", "loop_wide4_step", "wide4_amplification", "wide4_stable_dt",
+    "wide4_step",
 ]
 
 __version__ = "0.1.0"

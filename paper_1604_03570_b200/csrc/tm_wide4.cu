@@ -38,12 +38,17 @@ struct W4Args {
     double c0, c1, c2, c3, c4;
     double d0, d1, d2, dtD;  // 1/dx^2 per direction, D*dt
     int32_t box_x, box_y, stage_elems;
+    // SCATTER: face neighbours nbr[slot][-x,+x,-y,+y,-z,+z] (local slot, or < 0: none) and the
+    // uniform box extents; cells within 4 of a face are also written into the neighbour's
+    // ghost layers of the new field, so the next step needs no FillBoundary
+    const int32_t *nbr;
+    int32_t nxb, nyb, nzb;
 };
 
 // PAIR: lane l owns the adjacent cells 2l, 2l+1 (widths 34..64): the x window of both
 // cells is five 16-B shared loads and every y neighbour pair one, instead of a
 // scalar load per neighbour per cell.
-template <int CPL, int NWARP, bool PAIR = false>
+template <int CPL, int NWARP, bool PAIR = false, bool SCATTER = false>
 __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     wide4_kernel(const __grid_constant__ CUtensorMap map, W4Args a) {
     using namespace tmk;
@@ -124,6 +129,40 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
         double *const orow = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)r * st.row;
         uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane + (int64_t)c.y0 * st.row + c.x0 +
                                    (PAIR ? 2 * lane : lane));
+        // scatter targets (pointer deltas from the cell's own address), fixed per column
+        int64_t dx[CPL], dy = 0, dzl = 0, dzh = 0;
+        bool sx_on[CPL], sy_on = false, szl = false, szh = false;
+        int zrel = 0;
+        if constexpr (SCATTER) {
+            const int32_t *nb = a.nbr + 6 * c.slot;
+            const int ng = a.L.nghost;
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+                const int xr = c.x0 - a.L.xoff + (PAIR ? 2 * lane + j : lane + 32 * j);
+                sx_on[j] = false;
+                dx[j] = 0;
+                if (xr < kR && nb[0] >= 0) {
+                    sx_on[j] = true;
+                    dx[j] = (int64_t)(nb[0] - c.slot) * st.slot + a.nxb;
+                } else if (xr >= a.nxb - kR && nb[1] >= 0) {
+                    sx_on[j] = true;
+                    dx[j] = (int64_t)(nb[1] - c.slot) * st.slot - a.nxb;
+                }
+            }
+            const int yr = c.y0 - ng + r;
+            if (yr < kR && nb[2] >= 0) {
+                sy_on = true;
+                dy = (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)a.nyb * st.row;
+            } else if (yr >= a.nyb - kR && nb[3] >= 0) {
+                sy_on = true;
+                dy = (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)a.nyb * st.row;
+            }
+            szl = nb[4] >= 0;
+            szh = nb[5] >= 0;
+            dzl = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)a.nzb * st.plane;
+            dzh = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)a.nzb * st.plane;
+            zrel = c.z0 - ng + sg.k0;
+        }
 
         // window w[m] = u at plane k-4+m of this lane's cells; prime with planes k0-4 .. k0+3
         double w[2 * kR + 1][CPL];
@@ -210,6 +249,32 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
                 for (int j = 0; j < CPL; ++j)
                     if (on[j]) orow[koff + 32 * j] = out[j];
             }
+            if constexpr (SCATTER) {
+                double *const cell = orow + koff;
+                const bool zl = szl && zrel < kR, zh = szh && zrel >= a.nzb - kR;
+                if constexpr (PAIR) {
+                    if (on[1]) {
+                        const double2 pr = make_double2(out[0], out[1]);
+                        if (sy_on) *reinterpret_cast<double2 *>(cell + dy) = pr;
+                        if (zl) *reinterpret_cast<double2 *>(cell + dzl) = pr;
+                        if (zh) *reinterpret_cast<double2 *>(cell + dzh) = pr;
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            if (sx_on[j]) cell[j + dx[j]] = out[j];
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < CPL; ++j) {
+                        if (!on[j]) continue;
+                        double *const cj = cell + 32 * j;
+                        if (sy_on) cj[dy] = out[j];
+                        if (zl) cj[dzl] = out[j];
+                        if (zh) cj[dzh] = out[j];
+                        if (sx_on[j]) cj[dx[j]] = out[j];
+                    }
+                }
+                ++zrel;
+            }
             koff += pstep;
 #pragma unroll
             for (int m = 0; m < 2 * kR; ++m)
@@ -220,9 +285,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, 1)
     }
 }
 
-template <int CPL, int NWARP, bool PAIR = false>
+template <int CPL, int NWARP, bool PAIR = false, bool SCATTER = false>
 int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = wide4_kernel<CPL, NWARP, PAIR>;
+    auto kern = wide4_kernel<CPL, NWARP, PAIR, SCATTER>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -237,24 +302,38 @@ int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int nco
 
 }  // namespace
 
-extern "C" {
+namespace {
 
-int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
-                   int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
-                   double dtD, void *stream) {
+template <bool SCATTER>
+int wide4_dispatch(const CUtensorMap &map, const W4Args &a, const tm_march_plan *p, int ncomp, size_t smem,
+                   cudaStream_t s) {
+    const int cpl = (p->max_nx + 31) / 32;
+    if (cpl == 1) return launch_wide4_one<1, 16, false, SCATTER>(map, a, p->nctas, ncomp, smem, s);
+    if (cpl == 2 && p->even) return launch_wide4_one<2, 16, true, SCATTER>(map, a, p->nctas, ncomp, smem, s);
+    if (cpl == 2) return launch_wide4_one<2, 16, false, SCATTER>(map, a, p->nctas, ncomp, smem, s);
+    if (p->max_ny > 8) return tmk::fail(TM_ERR_INVALID, "tm_wide4_march: columns wider than 64 must be <= 8 rows");
+    return launch_wide4_one<4, 8, false, SCATTER>(map, a, p->nctas, ncomp, smem, s);
+}
+
+int wide4_common(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
+                 const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2, double dtD, const int32_t *d_nbr,
+                 const int32_t *box_extents, void *stream, const char *who) {
     using namespace tmk;
-    if (!p) return fail(TM_ERR_INVALID, "tm_wide4_march: null plan");
-    int rc = check_layout(layout, "tm_wide4_march");
+    if (!p) return fail(TM_ERR_INVALID, std::string(who) + ": null plan");
+    int rc = check_layout(layout, who);
     if (rc) return rc;
     const tm_layout &L = *layout;
     if (L.nghost < kR || !uold || !unew || uold == unew || !coeffs5)
-        return fail(TM_ERR_INVALID, "tm_wide4_march: needs nghost >= 4, distinct old/new fields and 5 coefficients");
-    if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_wide4_march: bad ncomp");
+        return fail(TM_ERR_INVALID,
+                    std::string(who) + ": needs nghost >= 4, distinct old/new fields and 5 coefficients");
+    if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, std::string(who) + ": bad ncomp");
     if (strides_of(L).comp >= ((int64_t)1 << 32))
-        return fail(TM_ERR_INVALID, "tm_wide4_march: one component of a slot must hold < 2^32 doubles");
+        return fail(TM_ERR_INVALID, std::string(who) + ": one component of a slot must hold < 2^32 doubles");
+    if (d_nbr && (!box_extents || box_extents[0] < 2 * kR || box_extents[1] < 2 * kR || box_extents[2] < 2 * kR))
+        return fail(TM_ERR_INVALID, std::string(who) + ": fused halos need uniform boxes of at least 8^3 cells");
     if (p->ncols == 0) return TM_OK;
     if (p->max_nx > 128 || p->max_ny > 16)
-        return fail(TM_ERR_INVALID, "tm_wide4_march: columns must be <= 128 wide and <= 16 rows");
+        return fail(TM_ERR_INVALID, std::string(who) + ": columns must be <= 128 wide and <= 16 rows");
     W4Args a{};
     a.cols = p->d_cols;
     a.segs = p->d_segs;
@@ -273,19 +352,41 @@ int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold
     a.box_x = ((p->max_nx + 2 * kR) + 1) & ~1;  // TMA: inner box bytes a multiple of 16
     a.box_y = p->max_ny + 2 * kR;
     a.stage_elems = ((a.box_x * a.box_y + 15) / 16) * 16;
+    a.nbr = d_nbr;
+    if (d_nbr) {
+        a.nxb = box_extents[0];
+        a.nyb = box_extents[1];
+        a.nzb = box_extents[2];
+    }
     // + slack: idle lanes of a partial-width column read (never store) past their row
     const size_t smem = (size_t)kW4Stages * a.stage_elems * sizeof(double) + 2 * kW4Stages * sizeof(uint64_t) + 2048;
-    if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_wide4_march: column plane too large for shared memory");
+    if (smem > 220 * 1024)
+        return fail(TM_ERR_INVALID, std::string(who) + ": column plane too large for shared memory");
     CUtensorMap map;
     rc = encode_plane_map(&map, L, uold, a.box_x, a.box_y);
     if (rc) return rc;
     cudaStream_t s = as_stream(stream);
-    const int cpl = (p->max_nx + 31) / 32;
-    if (cpl == 1) return launch_wide4_one<1, 16>(map, a, p->nctas, ncomp_sweep, smem, s);
-    if (cpl == 2 && p->even) return launch_wide4_one<2, 16, true>(map, a, p->nctas, ncomp_sweep, smem, s);
-    if (cpl == 2) return launch_wide4_one<2, 16>(map, a, p->nctas, ncomp_sweep, smem, s);
-    if (p->max_ny > 8) return fail(TM_ERR_INVALID, "tm_wide4_march: columns wider than 64 must be <= 8 rows");
-    return launch_wide4_one<4, 8>(map, a, p->nctas, ncomp_sweep, smem, s);
+    return d_nbr ? wide4_dispatch<true>(map, a, p, ncomp_sweep, smem, s)
+                 : wide4_dispatch<false>(map, a, p, ncomp_sweep, smem, s);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                   int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                   double dtD, void *stream) {
+    return wide4_common(p, layout, uold, unew, ncomp_sweep, coeffs5, dxi2_0, dxi2_1, dxi2_2, dtD, nullptr, nullptr,
+                        stream, "tm_wide4_march");
+}
+
+int tm_wide4_march_fused(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                         int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                         double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream) {
+    if (!d_nbr) return tmk::fail(TM_ERR_INVALID, "tm_wide4_march_fused: null neighbour table");
+    return wide4_common(p, layout, uold, unew, ncomp_sweep, coeffs5, dxi2_0, dxi2_1, dxi2_2, dtD, d_nbr,
+                        box_extents, stream, "tm_wide4_march_fused");
 }
 
 }  // extern "C"

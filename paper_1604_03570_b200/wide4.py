@@ -10,6 +10,12 @@ bits); the update itself is ONE launch of Kernel W (``tm_wide4_march``,
 csrc/tm_wide4.cu) over every box this rank owns, bit-identical to the
 reference per cell.  It reuses the FillBoundary plan and kernel unchanged:
 callers fill 4 ghost layers first, exactly as with the reference.
+
+``Wide4Runner`` is the reference's step loop (fill_boundary; wide4_step)
+on the device: with uniform boxes of at least 8^3 its steps are ONE launch
+each (``tm_wide4_march_fused``: the epilogue writes the 4-deep face ghosts of
+the next step, so the loop needs no FillBoundary), replayed from a CUDA graph
+of step pairs; one regular FillBoundary closes each ``advance``.
 """
 
 from __future__ import annotations
@@ -145,3 +151,108 @@ def loop_wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusiv
     same kernel."""
     _check(mf_new, mf_old)
     _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)
+
+
+class Wide4Runner:
+    """Owns an old/new pair and advances the wide4 diffusion ``n`` steps at a
+    time; bit-identical to ``steps x (fill_boundary; wide4_step)``.  Fused
+    (default when eligible): one launch per step, face ghosts written by the
+    previous step's epilogue; unfused: FillBoundary + Kernel W per step."""
+
+    def __init__(self, mf: MultiFab, geom: Geometry, diffusivity: float, dt: float,
+                 coeffs: StencilCoeffs8 | None = None, fused: bool | None = None,
+                 use_graph: bool | None = None):
+        import torch
+
+        from .march import face_neighbors, fusable
+        from .multifab import comm_info
+
+        if mf.nghost < RADIUS or mf.ncomp != 1:
+            raise ValueError("wide4 runner needs a single-component MultiFab with nghost >= 4")
+        self.geom, self.diffusivity, self.dt = geom, diffusivity, dt
+        self.coeffs = coeffs if coeffs is not None else derive_coeffs8()
+        self.a = mf
+        self.b = mf.clone_empty()
+        world = comm_info()[1]
+        ext = {mf.units[u].valid.extents for u in mf.local_units}
+        can_fuse = (world == 1 and fusable(mf, geom) and len(ext) == 1 and min(next(iter(ext))) >= 2 * RADIUS)
+        if fused and not can_fuse:
+            raise ValueError("fused wide4 needs one rank and uniform boxes of at least 8^3 covering the domain")
+        self.fused = can_fuse if fused is None else fused
+        self.use_graph = (world == 1) if use_graph is None else (use_graph and world == 1)
+        if self.fused:
+            self.nbr = torch.as_tensor(face_neighbors(mf, geom).reshape(-1), dtype=torch.int32, device=mf.device)
+            self.box = (ctypes.c_int32 * 3)(*next(iter(ext)))
+        self._graph = None
+        self._primed = False
+        self.steps_done = 0
+
+    @property
+    def current(self) -> MultiFab:
+        return self.a if self.steps_done % 2 == 0 else self.b
+
+    def reset(self) -> None:
+        """Call after modifying ``a`` from outside: restart at step 0."""
+        self.steps_done = 0
+        self._primed = False
+
+    def close(self) -> None:
+        self._graph = None
+
+    def _step(self, old: MultiFab, new: MultiFab) -> None:
+        from .multifab import fill_boundary
+
+        if not self.fused:
+            fill_boundary(old, self.geom)
+            wide4_step(new, old, self.geom, self.diffusivity, self.dt, coeffs=self.coeffs)
+            return
+        c = self.coeffs
+        dxi2 = tuple(1.0 / d ** 2 for d in self.geom.dx)
+        plan = wide4_plan(old)
+        cbuf = (ctypes.c_double * 5)(c.c0, c.c1, c.c2, c.c3, c.c4)
+        _native.check(_native.load().tm_wide4_march_fused(
+            plan.handle, old.layout.to_c(), old.ptr, new.ptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
+            dxi2[0], dxi2[1], dxi2[2], self.diffusivity * self.dt, self.nbr.data_ptr(), self.box, old.stream()),
+            "tm_wide4_march_fused")
+
+    def _capture(self) -> None:
+        import torch
+
+        self._step(self.a, self.b)  # warm plans and tensor maps outside capture
+        self._step(self.b, self.a)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
+            self._step(self.a, self.b)
+            self._step(self.b, self.a)
+        torch.cuda.current_stream().wait_stream(s)
+        self._graph = g
+
+    def advance(self, n: int, finalize: bool = True) -> MultiFab:
+        """Advance ``n`` steps; returns the MultiFab holding the state (all
+        ghosts filled when ``finalize``)."""
+        from .multifab import fill_boundary
+
+        if self.fused and not self._primed:
+            fill_boundary(self.current, self.geom)
+            self._primed = True
+        k = 0
+        if self.use_graph and self.steps_done % 2 == 0 and n >= 2:
+            if self._graph is None:
+                self._capture()  # two real steps
+                self.steps_done += 2
+                k += 2
+            while n - k >= 2:
+                self._graph.replay()
+                self.steps_done += 2
+                k += 2
+        while k < n:
+            old, new = (self.a, self.b) if self.steps_done % 2 == 0 else (self.b, self.a)
+            self._step(old, new)
+            self.steps_done += 1
+            k += 1
+        if finalize:
+            fill_boundary(self.current, self.geom)
+        return self.current

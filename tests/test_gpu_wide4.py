@@ -182,3 +182,45 @@ def test_wide4_needs_four_ghosts(tm):
     mf2 = tm.MultiFab(tm.BoxArray([dom]), 2, 4)
     with pytest.raises(ValueError):
         tm.wide4_step(mf2.clone_empty(), mf2, geom, 1.0, 1e-5, None)
+
+
+@pytest.mark.parametrize("n,mgs,steps,graph", [
+    (64, 32, 5, True),     # 2^3 boxes of 32^3: 2 cells per lane (adjacent pair), odd step count
+    (40, 40, 4, False),    # one 40^3 box: every face its own periodic image
+    (48, 16, 3, True),     # 3^3 boxes of 16^3
+    (24, 8, 6, True),      # 8^3 boxes: the 4-deep faces of a box cover it completely
+    (96, 96, 2, False),    # 96 wide: 3 cells per lane... routed to 4 per lane, 8-row columns
+])
+def test_fused_wide4_runner_matches_oracle(tm, n, mgs, steps, graph):
+    """One launch per step (FillBoundary fused into the epilogue) against the
+    whole-domain oracle and against the reference-structured unfused loop."""
+    w = dataclasses.replace(tm.CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
+    glob = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    dt = tm.wide4_stable_dt(1.0, (w.dx,) * 3)
+    coeffs = tm.derive_coeffs8()
+    outs = []
+    for fused in (True, False):
+        mf = tm.MultiFab(ba, 1, 4)
+        mf.from_global(glob)
+        r = tm.Wide4Runner(mf, geom, 1.0, dt, coeffs, fused=fused, use_graph=graph)
+        assert r.fused == fused
+        outs.append(r.advance(steps).to_global().cpu().numpy()[0])
+        r.close()
+    want = orc.wide4_periodic(glob[0], steps, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[1], want)
+
+
+def test_fused_wide4_eligibility(tm):
+    dom = tm.Box((0, 0, 0), (23, 23, 23))
+    geom = tm.Geometry(dom, (True, True, True), (1.0 / 24,) * 3)
+    small = tm.MultiFab(tm.BoxArray.chop(dom, 6), 1, 4)  # 6^3 boxes: 4-deep faces would overlap
+    assert not tm.Wide4Runner(small, geom, 1.0, 1e-6).fused
+    with pytest.raises(ValueError):
+        tm.Wide4Runner(small, geom, 1.0, 1e-6, fused=True)
+    dom23 = tm.Box((0, 0, 0), (22, 22, 22))
+    geom23 = tm.Geometry(dom23, (True, True, True), (1.0 / 23,) * 3)
+    ragged = tm.MultiFab(tm.BoxArray.chop(dom23, 10), 1, 4)  # 8, 8, 7 cells: not uniform
+    assert not tm.Wide4Runner(ragged, geom23, 1.0, 1e-6).fused

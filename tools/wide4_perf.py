@@ -1,6 +1,7 @@
 """wide4 throughput on a C2-shaped problem (256^3, 64^3 boxes, nghost 4):
 Kernel W alone, FillBoundary (4 ghost layers) alone, and the reference step
-(FB + wide4).  python tools/wide4_perf.py [n mgs] [--rows R --nctas N]"""
+(FB + wide4), and the fused step (Wide4Runner: one launch, face ghosts written
+by the epilogue).  python tools/wide4_perf.py [n mgs] [--rows R --nctas N]"""
 
 import dataclasses
 import os
@@ -34,11 +35,16 @@ def main():
     fb = graph_time(lambda: tm.fill_boundary(a, geom, plan), 10)
     step = graph_time(lambda: (tm.fill_boundary(a, geom, plan), _launch(b, a, geom, 1.0, dt, co, rows, nctas),
                                tm.fill_boundary(b, geom, plan), _launch(a, b, geom, 1.0, dt, co, rows, nctas)), 5) / 2
+    r = tm.Wide4Runner(a, geom, 1.0, dt, co, fused=True)
+    r.advance(2)
+    fused = graph_time(lambda: (r._step(r.a, r.b), r._step(r.b, r.a)), 5) / 2
+    r.close()
     cells = w.cells
     ghosts = sum(t.dst_box.ncells for t in plan.tags)
     print(f"wide4 {n}^3 mgs {mgs}: kernel {kern * 1e3:.1f} us ({cells / kern / 1e6:.1f} G cell/s, "
           f"{16 * cells / kern / 1e6:.0f} GB/s alg) | FB {fb * 1e3:.1f} us ({ghosts} ghost cells, "
-          f"{16 * ghosts / fb / 1e6:.0f} GB/s) | step {step * 1e3:.1f} us ({cells / step / 1e6:.1f} G cell/s)")
+          f"{16 * ghosts / fb / 1e6:.0f} GB/s) | step {step * 1e3:.1f} us ({cells / step / 1e6:.1f} G cell/s) | "
+          f"fused step {fused * 1e3:.1f} us ({cells / fused / 1e6:.1f} G cell/s)")
 
 
 if __name__ == "__main__":
