@@ -448,6 +448,29 @@ __global__ void __launch_bounds__((kFsWarps + 1) * 32, 1)
         }
 #pragma unroll
         for (int j = 0; j < kFsChunks; ++j) inc[j] = warp_incl_scan(ls[j].P, lane);
+        // the whole stage folded into one test: total, and min / max over every value of
+        // (prefix + floor) relative to the stage start -- so the ordered hand-off below is
+        // one comparison per warp unless the stage needs the chunk-by-chunk path
+        int64_t stot = 0, slo = INT64_MAX, shi = INT64_MIN;
+        bool sbad = false;
+        if (spec) {
+#pragma unroll
+            for (int j = 0; j < kFsChunks; ++j) {
+                if (j * 256 + lane * 8 < cnt) {
+                    const int64_t base_l = stot + inc[j] - ls[j].P;
+                    slo = min(slo, base_l + ls[j].lo);
+                    shi = max(shi, base_l + ls[j].hi);
+                    sbad |= ls[j].bad;
+                }
+                stot += __shfl_sync(0xffffffffu, inc[j], 31);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                slo = min(slo, (int64_t)__shfl_xor_sync(0xffffffffu, slo, o));
+                shi = max(shi, (int64_t)__shfl_xor_sync(0xffffffffu, shi, o));
+            }
+            sbad = __any_sync(0xffffffffu, sbad);
+        }
         // T = +0 (a zero field's start): does the stage hold only +-0?  Then T stays +0.
         bool zeros = false;
         if (active && __double_as_longlong(Tbase) == 0) {
@@ -472,7 +495,12 @@ __global__ void __launch_bounds__((kFsWarps + 1) * 32, 1)
             double sc2, q2;
             bool neg2;
             int64_t K;
-            if (spec && fast_range(T, sc2, q2, neg2, K) && sc2 == scale && neg2 == neg) {
+            const bool same = spec && fast_range(T, sc2, q2, neg2, K) && sc2 == scale && neg2 == neg;
+            if (same && !sbad && K + slo >= kKLo && K + shi <= kKHi) {
+                jf = kFsChunks;  // the common case: the whole stage at once
+                K += stot;
+                T = from_units(K, q, neg);
+            } else if (same) {
                 jf = kFsChunks;
 #pragma unroll
                 for (int j = 0; j < kFsChunks; ++j) {
