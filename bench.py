@@ -359,7 +359,8 @@ def run_ours(args, w):
     # checksum), alternating between two runners/streams so one job's PCIe
     # copies overlap the other's steps; host reads after the last job.
     pipe = None
-    if not args.no_pipeline:
+    # one GPU only: concurrent graphs on two streams must not interleave one NCCL communicator
+    if not args.no_pipeline and world == 1:
         runner2 = HeatRunner(mf.clone_empty(), geom, params, sched, plan, use_graph=runner.use_graph,
                              zmerge=args.zmerge, fused=runner.fused)
         runners = [runner, runner2]
