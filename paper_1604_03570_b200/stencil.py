@@ -58,6 +58,32 @@ def _schedule_for(mf: MultiFab, schedule):
     return schedule
 
 
+# Which kernel runs heat_step's sweep.  The tiling never changes a result
+# (reference test_kernels.py:259-283), so large problems go to the persistent
+# column march (Kernel A2 with x halos from the ghost columns: C2 61 us vs 64-68
+# us for the tile kernel) and small ones, or zmerge requests, to the tile
+# kernel.  "tiled" / "march" force one (tests).
+SWEEP_KERNEL = "auto"
+MARCH_MIN_CELLS = 1 << 21
+
+
+def _use_march(mf: MultiFab, zmerge: bool) -> bool:
+    from .march import march_eligible
+
+    if SWEEP_KERNEL == "tiled" or zmerge:
+        return False
+    if not march_eligible(mf):
+        if SWEEP_KERNEL == "march":
+            raise ValueError("column march needs boxes of even x extent <= 128")
+        return False
+    if SWEEP_KERNEL == "march":
+        return True
+    big = mf._plans.get("march_big")
+    if big is None:
+        big = mf._plans["march_big"] = sum(mf.units[u].valid.ncells for u in mf.local_units) * mf.ncomp >= MARCH_MIN_CELLS
+    return big
+
+
 def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatParams,
               schedule: TileSchedule | None = None, workers: int = 1, arenas=None, verify: bool = False,
               zmerge: bool = False) -> None:
@@ -79,6 +105,11 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
         raise ValueError("heat_step needs distinct old/new MultiFabs (double buffering)")
     if verify and params.dt > params.stability_limit:
         warnings.warn(f"dt={params.dt} exceeds stability bound {params.stability_limit}", stacklevel=2)
+    if _use_march(mf_old, zmerge):
+        from .march import heat_march
+
+        heat_march(mf_new, mf_old, params)
+        return
     sched = _schedule_for(mf_old, schedule)
     plan = schedule_sweep_plan(mf_old, sched, zmerge)
     if plan.nblocks == 0:

@@ -136,9 +136,13 @@ def test_heat_matches_reference_golden(tm):
         assert [mf.reduce_min(c) for c in range(w.ncomp)] == list(z[name + "/min"])
 
 
-@pytest.mark.parametrize("tiling,zmerge", [("off", False), ((16, 4, 4), False), ((1024, 8, 8), True),
-                                           ((5, 3, 7), False), ((64, 64, 1), True)])
-def test_heat_tiling_invariance(tm, tiling, zmerge):
+@pytest.mark.parametrize("tiling,zmerge,kernel", [("off", False, "auto"), ((16, 4, 4), False, "auto"),
+                                                  ((1024, 8, 8), True, "auto"), ((5, 3, 7), False, "auto"),
+                                                  ((64, 64, 1), True, "auto"), ((16, 4, 4), False, "march")])
+def test_heat_tiling_invariance(tm, tiling, zmerge, kernel, monkeypatch):
+    from paper_1604_03570_b200 import stencil
+
+    monkeypatch.setattr(stencil, "SWEEP_KERNEL", kernel)
     w = tm.CONFIGS["C1"].scaled(48, 24, 4)
     glob = tm.make_init(w)
     got = run_device(tm, w, 4, glob, tiling=tiling, zmerge=zmerge).to_global().cpu().numpy()
@@ -163,12 +167,20 @@ def test_heat_big_untiled_box_is_split(tm):
     assert np.array_equal(got, orc.heat_periodic(glob, 1, p[:3], p[3]))
 
 
-def test_heat_c2_full_size(tm):
+@pytest.mark.parametrize("kernel", ["auto", "tiled"])
+def test_heat_c2_full_size(tm, kernel, monkeypatch):
+    """heat_step at C2 size: auto routes to the column march, "tiled" keeps
+    the tile kernel covered at full size."""
+    from paper_1604_03570_b200 import stencil
+
+    monkeypatch.setattr(stencil, "SWEEP_KERNEL", kernel)
     w = tm.CONFIGS["C2"]
     glob = tm.make_init(w)
     p = tm.HeatParams.stable(1.0, (w.dx,) * 3).coefficients()
     mf = run_device(tm, w, 3, glob)
     assert np.array_equal(mf.to_global().cpu().numpy(), orc.heat_periodic(glob, 3, p[:3], p[3]))
+    if kernel == "tiled":
+        return
     # full 100 steps: the flux form conserves the checksum
     s0 = float(np.sum(glob))
     mf = run_device(tm, w, w.steps, glob)
