@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 
@@ -18,6 +19,15 @@ int fail(int code, const std::string &msg);
 int cuda_fail(cudaError_t e, const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Programmatic dependent launch for the step kernels (TM_PDL=0 turns it off).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = getenv("TM_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 // element strides of a layout
 struct Strides {
@@ -152,6 +162,13 @@ __device__ __forceinline__ void tma_load_plane_hint(void *dst, const CUtensorMap
 __device__ __forceinline__ void prefetch_tensormap(const CUtensorMap *map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
+
+// Programmatic dependent launch: a kernel launched with the programmatic
+// stream-serialization attribute may start its prologue while the previous
+// kernel on the stream drains; grid_dep_wait() blocks until that kernel has
+// completed and its writes are visible (a no-op without the attribute).
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // L2 eviction-priority policies for stores (createpolicy + st.global.L2::cache_hint)
 __device__ __forceinline__ uint64_t policy_evict_last() {

@@ -33,7 +33,13 @@ using tmk::Segment;
 
 // TMA ring depth (powers of two: stage and phase come from the plane counter by mask/shift).
 // (8 heat stages measured: C2 62.6 us vs 56.9 us at 4 -- fewer CTAs fit; C3/C5 within +-3 %.)
-constexpr int kHeatStages = 4;
+#ifndef TM_HEAT_STAGES
+#define TM_HEAT_STAGES 4
+#endif
+constexpr int kHeatStages = TM_HEAT_STAGES;
+#ifndef TM_MARCH_EXPERIMENT
+#define TM_MARCH_EXPERIMENT 0
+#endif
 constexpr int kGsrbStages = 4;
 
 struct MarchArgs {
@@ -105,7 +111,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         }
         fence_mbar_init();
     }
+    grid_dep_launch();  // the next step's CTAs may take SM slots as ours retire
     __syncthreads();
+    grid_dep_wait();  // previous step complete: its unew is our uold, its uold our unew
 
     if (warp == NWARP) {  // ---------------- producer warp ----------------
         if (lane == 0) {
@@ -297,7 +305,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                     const double fzp = REV ? fzm[i][j] : fnew, fzn = REV ? fnew : fzm[i][j];
                     double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
                     sum = rn_add(sum, rn_mul(rn_sub(fzp, fzn), c2));
+#if TM_MARCH_EXPERIMENT == 1  // data movement only (timing experiments; wrong results)
+                    out[i][j] = u0;
+#else
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
+#endif
                     fzm[i][j] = fnew;
                 }
             }
@@ -315,6 +327,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 if (!on[i]) continue;
+#if TM_MARCH_EXPERIMENT == 2  // no stores (timing experiments; wrong results)
+                if (out[i][0] != 1234.5) continue;
+#endif
                 st_cells(orow[i] + koff, i);
                 if (SCATTER) {
                     if (i == ylo_i) st_cells(ylo + koff, i);
@@ -627,8 +642,18 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const Marc
         if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(march)");
         configured = true;
     }
-    kern<<<dim3(nctas, ncomp), (NWARP + 1) * 32, smem, s>>>(map, xmap, a);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nctas, ncomp);
+    cfg.blockDim = dim3((NWARP + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = tmk::pdl_enabled() ? 1 : 0;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, xmap, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march launch");
     return TM_OK;
 }

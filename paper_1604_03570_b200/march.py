@@ -18,6 +18,8 @@ Host side of ``csrc/tm_march.cu``:
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _native
@@ -26,7 +28,7 @@ from .boxarray import BoxIndex, Geometry
 from .multifab import MultiFab, cell_offsets
 
 SMEM_BUDGET = 220 * 1024
-STAGES = 4        # heat ring depth (tm_march.cu kHeatStages)
+STAGES = int(os.environ.get("TM_HEAT_STAGES", "4"))  # heat ring depth (tm_march.cu kHeatStages; same -D)
 GSRB_STAGES = 4   # GSRB ring depth (kGsrbStages)
 
 

@@ -7,7 +7,10 @@ Per heat config: fused and unfused step paths (independent kernels) must agree
 bit for bit; each component's sum is conserved (flux form) to 1e-11
 relative; C1/C2 checksums equal the reference's (golden / SURVEY value).
 C4 (GSRB): residual decreases; with --oracle the final phi and residual are
-compared bit for bit with the whole-domain numpy restatement.
+compared bit for bit with the whole-domain numpy restatement.  With --oracle
+the heat configs also run the reference path restated in C (oracle/tm_oracle.c,
+OpenMP) at full size and compare every valid cell and each component's serial
+checksum bit for bit with the device result.
 Prints one JSON line per config.
 """
 
@@ -37,7 +40,52 @@ def ev_time(fn):
     return e0.elapsed_time(e1) * 1e-3
 
 
-def heat_config(name):
+def oracle_heat(name, w, glob, ba, geom, plan, p):
+    """The reference path restated in C (oracle/tm_oracle.c: tag FillBoundary +
+    per-component heat_tiles, OpenMP over all host threads) at full size.
+    Returns the host MultiFab holding the final field."""
+    from oracle import oracle as orc
+    from paper_1604_03570_b200.box import decompose
+
+    nt = orc.max_threads()
+    valids = list(ba)
+    old = orc.HostMF(valids, w.ncomp, w.nghost)
+    old.from_global(glob)
+    new = orc.HostMF(valids, w.ncomp, w.nghost)
+    tags = orc.tags_array(plan.tags)
+    tiles = orc.tiles_array([(u, t) for u in range(len(valids)) for t in decompose(valids[u], w.tile_size)])
+    c = p.coefficients()
+    for _ in range(w.steps):
+        orc.fill_boundary(old, tags, nt)
+        orc.heat_step(new, old, tiles, c[:3], c[3], nt)
+        old, new = new, old
+    del new
+    return old, nt
+
+
+def compare_with_oracle(res, out_global, host, ba, w):
+    """Bit-compare every valid cell of the device result with the oracle's, box by box."""
+    from oracle import oracle as orc
+
+    bad = 0
+    maxdiff = 0.0
+    for u, v in enumerate(ba):
+        sl = tuple(slice(v.lo[d], v.hi[d] + 1) for d in (2, 1, 0))
+        for c in range(w.ncomp):
+            d = out_global[(c,) + sl].cpu().numpy()
+            h = host.valid_view(u, c).transpose(2, 1, 0)
+            if not np.array_equal(d, h):
+                bad += 1
+                maxdiff = max(maxdiff, float(np.max(np.abs(d - h))))
+    res["phi_equals_oracle"] = bad == 0
+    res["oracle_mismatched_box_comps"] = bad
+    if bad:
+        res["oracle_max_abs_diff"] = maxdiff
+    res["oracle_sums"] = [orc.reduce_sum(host, c) for c in range(w.ncomp)]
+    res["sums_equal_oracle"] = res["oracle_sums"] == res["fused_sums"]
+
+
+def heat_config(name, oracle=False):
     w = tm.CONFIGS[name]
     t0 = time.time()
     glob = tm.make_init(w)
@@ -49,6 +97,11 @@ def heat_config(name):
     plan = tm.build_fill_plan(mf, geom)
     t_plan = time.time() - t0
     g = torch.from_numpy(glob).cuda()
+    host = None
+    if oracle:
+        t0 = time.time()
+        host, nt = oracle_heat(name, w, glob, ba, geom, plan, tm.HeatParams.stable(1.0, geom.dx))
+        res_oracle = {"oracle_s": time.time() - t0, "oracle_threads": nt}
     del glob
     sums0 = [float(torch.sum(g[c]).item()) for c in range(w.ncomp)]
     p = tm.HeatParams.stable(1.0, geom.dx)
@@ -71,6 +124,9 @@ def heat_config(name):
         del r
         torch.cuda.empty_cache()
     res["fused_equals_unfused"] = bool(torch.equal(finals["fused"], finals["unfused"]))
+    if host is not None:
+        res.update(res_oracle)
+        compare_with_oracle(res, finals["fused"], host, ba, w)
     res["conservation_max_rel"] = max(abs(s - s0) / abs(s0) for s, s0 in zip(res["fused_sums"], sums0))
     if name in REF_SUMS:
         res["checksum_equals_reference"] = res["fused_sums"][0] == REF_SUMS[name]
@@ -122,7 +178,7 @@ def main():
     torch.cuda.set_device(0)
     for n in names:
         t0 = time.time()
-        res = gsrb_config("--oracle" in sys.argv) if n == "C4" else heat_config(n)
+        res = gsrb_config("--oracle" in sys.argv) if n == "C4" else heat_config(n, "--oracle" in sys.argv)
         res["wall_s"] = time.time() - t0
         print(json.dumps(res), flush=True)
         torch.cuda.empty_cache()
