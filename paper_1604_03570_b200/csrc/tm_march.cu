@@ -72,7 +72,9 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
         tma_load_plane(stage, map, bar, c.x0, c.y0 - 1, z, w);
         // x halo: y range of the column, both sides, valid plane z - nghost
         const int g = a.L.nghost;
+#if TM_MARCH_EXPERIMENT != 3  // 3: skip the x-halo copy (timing experiment; wrong results)
         tma_load_plane(stage + a.xh_off, xmap, bar, c.y0 - g, 0, z - g, w);
+#endif
     } else {
         tma_load_plane(stage, map, bar, (c.x0 - 1) & ~1, c.y0 - 1, z, w);
     }
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bx = a.box_x;
     const uint32_t tx_bytes =
-        (uint32_t)((a.box_x * a.box_y + (PACKED ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
+        (uint32_t)((a.box_x * a.box_y + (PACKED && TM_MARCH_EXPERIMENT != 3 ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
 
     if (tid == 0) {
         prefetch_tensormap(&map);
