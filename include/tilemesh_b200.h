@@ -176,8 +176,9 @@ int tm_gsrb_march(tm_march_plan *plan, const tm_layout *phi_layout, double *phi,
                   const double *rhs, int32_t color, double h2, double *xh, const int32_t *d_nbr, void *stream);
 
 /* ---- GSRB on colour-split storage (during a solve) ---------------------------
- * Each colour of phi in its own array [slot][z+1][y+1][i+2] (rows nx/2 + 4
- * doubles; entry i of row (y, z) = cell x = 2i + ((c + parity + y + z) & 1),
+ * Each colour of phi in its own array [slot][z+1][y+1][i+4] (rows nx/2 + 8
+ * doubles, so valid entries start on 32-B sectors; entry i of row (y, z) =
+ * cell x = 2i + ((c + parity + y + z) & 1),
  * i in [-1, nx/2]), rhs split into [slot][z][y][nx/2] per colour.  A colour
  * pass reads only the other colour and writes only its own: 24 bytes per
  * UPDATED cell.  Same per-cell form as tm_gsrb_color (bit-identical); the

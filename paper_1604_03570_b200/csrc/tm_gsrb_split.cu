@@ -31,9 +31,15 @@ using tmk::Segment;
 
 constexpr int kSStages = 4;
 
+// Entry e of a colour row sits at index e + kE0 of a row of wp = nx/2 + 8 doubles
+// (320 B for 64-wide boxes): every row's valid entries start on a 32-B sector
+// boundary, so a pass writes whole sectors (no partial-sector write-back);
+// TMA loads rows from entry -2 (index 2, 16-B aligned), nx/2 + 4 doubles wide.
+constexpr int kE0 = 4;
+
 struct ColourLayout {
     int32_t nslots, nx, ny, nz;  // valid extents of every box
-    int32_t wp;                  // doubles per colour row: nx/2 + 4
+    int32_t wp;                  // doubles per colour row: nx/2 + 8
     int64_t row, plane, slot;    // strides of a colour array
     int64_t rrow, rplane, rslot; // strides of a colour rhs array (nx/2 per row, valid rows only)
 };
@@ -44,7 +50,7 @@ __host__ __device__ inline ColourLayout colour_layout(int nslots, int nx, int ny
     C.nx = nx;
     C.ny = ny;
     C.nz = nz;
-    C.wp = nx / 2 + 4;
+    C.wp = nx / 2 + 8;
     C.row = C.wp;
     C.plane = C.row * (ny + 2);
     C.slot = C.plane * (nz + 2);
@@ -74,7 +80,7 @@ __global__ void split_kernel(tm_layout L, const double *__restrict__ phi, Colour
             for (int c = 0; c < 2; ++c) {
                 const int o = (c + parity[slot] + y + z) & 1;
                 const int x = 2 * i + o;
-                double *dst = (c ? c1 : c0) + slot * C.slot + (int64_t)zz * C.plane + (int64_t)yy * C.row + (i + 2);
+                double *dst = (c ? c1 : c0) + slot * C.slot + (int64_t)zz * C.plane + (int64_t)yy * C.row + (i + kE0);
                 if (x >= -1 && x <= C.nx) *dst = prow[x];
                 if (rhs && valid_row && i >= 0 && i < nh) {
                     const double *rrow = rhs + slot * rs.slot + (int64_t)(z + R.nghost) * rs.plane +
@@ -101,7 +107,7 @@ __global__ void merge_kernel(tm_layout L, double *__restrict__ phi, ColourLayout
             for (int c = 0; c < 2; ++c) {
                 const int o = (c + parity[slot] + y + z) & 1;
                 prow[2 * i + o] =
-                    (c ? c1 : c0)[slot * C.slot + (int64_t)(z + 1) * C.plane + (int64_t)(y + 1) * C.row + (i + 2)];
+                    (c ? c1 : c0)[slot * C.slot + (int64_t)(z + 1) * C.plane + (int64_t)(y + 1) * C.row + (i + kE0)];
             }
         }
     }
@@ -131,7 +137,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
     const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
     if (s_begin >= s_end) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wp = C.wp, nh = C.nx / 2;
+    const int nh = C.nx / 2, wp = nh + 4;  // wp here: the staged row width (entries -2 .. nh+1)
     const int R = a.box_y - 2;
     const uint32_t tx_bytes = (uint32_t)((wp * a.box_y + nh * R) * (int)sizeof(double));
 
@@ -162,7 +168,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
                     const int zv = zv0 + sg.k0 - 1 + q;  // valid z of this plane (-1 .. nz)
                     mbar_arrive_expect_tx(&bars[st_i], tx_bytes);
                     // other colour: rows yv-1 .. yv+R (array rows yv .. yv+R+1), plane zv (array zv+1)
-                    tma_load_plane(stage, &omap, &bars[st_i], 0, yv, zv + 1, c.slot);
+                    tma_load_plane(stage, &omap, &bars[st_i], kE0 - 2, yv, zv + 1, c.slot);
                     // rhs of this colour (out-of-range halo planes read as zeros, never used)
                     tma_load_plane(stage + a.rhs_off, &rmap, &bars[st_i], 0, yv, zv, c.slot);
                 }
@@ -218,7 +224,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
             const int rc = min(r, R - 1);
             so[i] = (uint32_t)((rc + 1) * wp + ii + 2) * 8u;
             ro[i] = (uint32_t)(a.rhs_off + rc * nh + ii) * 8u;
-            orow[i] = a.out + c.slot * C.slot + (int64_t)(yv0 + r + 1) * C.row + (ii + 2);
+            orow[i] = a.out + c.slot * C.slot + (int64_t)(yv0 + r + 1) * C.row + (ii + kE0);
         }
         // z march state per cell: the other colour's value below (carried)
         double ob[RPW][CPL];
@@ -311,7 +317,7 @@ int encode_colour_map(CUtensorMap *map, const ColourLayout &C, const double *bas
     X.pitch = C.wp;
     X.ny = C.ny + 2;
     X.nz = C.nz + 2;
-    return tmk::encode_plane_map(map, X, base, C.wp, box_y);
+    return tmk::encode_plane_map(map, X, base, C.nx / 2 + 4, box_y);
 }
 
 int encode_colour_rhs_map(CUtensorMap *map, const ColourLayout &C, const double *base, int rows) {
@@ -380,7 +386,7 @@ int tm_gsrb_split_pass(tm_march_plan *p, int32_t nslots, int32_t nx, int32_t ny,
     a.color = color;
     a.h2 = h2;
     a.box_y = p->max_ny + 2;
-    a.rhs_off = ((a.C.wp * a.box_y + 15) / 16) * 16;
+    a.rhs_off = (((a.C.nx / 2 + 4) * a.box_y + 15) / 16) * 16;
     a.stage_elems = a.rhs_off + ((nx / 2 * p->max_ny + 15) / 16) * 16;
     const size_t smem = (size_t)kSStages * a.stage_elems * sizeof(double) + 2 * kSStages * sizeof(uint64_t);
     CUtensorMap omap, rmap;

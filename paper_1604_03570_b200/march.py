@@ -561,7 +561,7 @@ class SplitGSRB:
         self.nx, self.ny, self.nz = v.extents
         nh, n = self.nx // 2, len(phi.local_units)
         dev = phi.device
-        self.c = [torch.zeros((n, self.nz + 2, self.ny + 2, nh + 4), dtype=torch.float64, device=dev)
+        self.c = [torch.zeros((n, self.nz + 2, self.ny + 2, nh + 8), dtype=torch.float64, device=dev)
                   for _ in range(2)]
         self.r = [torch.zeros((n, self.nz, self.ny, nh), dtype=torch.float64, device=dev) for _ in range(2)]
         par = [sum(phi.units[u].valid.lo) & 1 for u in phi.local_units]
