@@ -403,6 +403,20 @@ class FusedHalo:
         table = face_neighbors(a, geom, multi)
         self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=a.device)
         self.plan = march_plan(a, True, max_rows, nctas)
+        # Multi-rank: the columns of boxes with a face on another rank ("boundary" boxes) march
+        # first; their faces travel on a side stream while the remaining columns march, so the
+        # NCCL exchange overlaps the interior sweep.  Each column is still
+        # computed exactly once, by the same kernel, so results do not change.
+        self.plan_b = self.plan_i = None
+        self.comm = None
+        if multi:
+            cols = self.plan.columns
+            bslots = np.nonzero((table == REMOTE).any(axis=1))[0]
+            isb = np.isin(cols["slot"], bslots)
+            if isb.any() and (~isb).any():
+                self.plan_b = _native.MarchPlan(cols[isb], self.plan.nctas)
+                self.plan_i = _native.MarchPlan(cols[~isb], self.plan.nctas)
+                self.comm = torch.cuda.Stream(a.device)
         # faces whose neighbour is on another rank: filled by the halo exchange after each
         # step; x faces then copied from the ghost column into the packed x halo
         remote_x = [(s, side) for s in range(table.shape[0]) for side in (0, 1) if table[s, side] == REMOTE]
@@ -436,23 +450,48 @@ class FusedHalo:
         walks the columns backwards (same results): alternating it between
         consecutive steps lets each step start on the planes the previous
         one wrote last, while they are still in L2."""
-        c = params.coefficients()
-        _native.check(_native.load().tm_heat_march(
-            self.plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
-            self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
-            old.stream()), "tm_heat_march(fused)")
-        if self.remote:  # faces shared with other ranks: NCCL exchange of the new field's boundary
-            from .fillplan import build_fill_plan
-            from .multifab import _device_fill
+        import torch
 
-            if self.fill_plan is None:
-                self.fill_plan = build_fill_plan(new, self.geom)
-            _, halo = _device_fill(new, self.fill_plan)
+        c = params.coefficients()
+
+        def march(plan):
+            _native.check(_native.load().tm_heat_march(
+                plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
+                self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
+                old.stream()), "tm_heat_march(fused)")
+
+        if not self.remote:
+            march(self.plan)
+            return
+        # faces shared with other ranks: NCCL exchange of the new field's boundary
+        from .fillplan import build_fill_plan
+        from .multifab import _device_fill
+
+        if self.fill_plan is None:
+            self.fill_plan = build_fill_plan(new, self.geom)
+        _, halo = _device_fill(new, self.fill_plan)
+
+        def exchange():
             stream = new.stream()
             halo.start(new, stream)
             halo.finish(new, stream)
             if self._remote_x is not None:
                 self._remote_x.run(self.xh[id(new)].data_ptr(), self.xh_side, new.ptr, new.layout.side(), stream)
+
+        if self.comm is None:  # every local box touches another rank: nothing to overlap with
+            march(self.plan)
+            exchange()
+            return
+        main = torch.cuda.current_stream(new.device)
+        march(self.plan_b)
+        # the exchange reads the boundary boxes' valid cells and writes only ghost cells of remote
+        # faces (and their x halos); the interior columns write other cells, so the two run
+        # concurrently; the next step waits for both
+        self.comm.wait_stream(main)
+        with torch.cuda.stream(self.comm):
+            exchange()
+        march(self.plan_i)
+        main.wait_stream(self.comm)
 
 
 class FusedGSRB:

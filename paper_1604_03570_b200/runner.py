@@ -77,9 +77,10 @@ class HeatRunner:
     @property
     def launches_per_step(self) -> int:
         if self.fused:
-            # multi-rank: march, pack, unpack (+ x-halo refresh when an x face is remote)
+            # multi-rank: march (boundary and interior columns as two launches when both
+            # exist), pack, unpack (+ x-halo refresh when an x face is remote)
             if self.fh.remote:
-                return 3 + (self.fh._remote_x is not None)
+                return 3 + (self.fh._remote_x is not None) + (self.fh.comm is not None)
             return 1
         # multi-rank: pack, local copies, interior sweep, unpack, boundary sweep
         return 5 if self.a.dm.nranks > 1 else 2

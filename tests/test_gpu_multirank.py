@@ -25,7 +25,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, out, fused):
+def worker(rank, world, port, out, fused, slabs=False):
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
@@ -36,7 +36,9 @@ def worker(rank, world, port, out, fused):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        w = tm.CONFIGS["C5"].scaled(48, 16, 4)  # 27 boxes, 2 comps, 2 ghosts
+        # 27 boxes split mid-layer, or 216 boxes = three z-layers per rank (the middle one
+        # has no remote face: its columns march while the boundary faces are exchanged)
+        w = tm.CONFIGS["C5"].scaled(48, 8 if slabs else 16, 4)  # 2 comps, 2 ghosts
         geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
         ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
         glob = tm.make_init(w)
@@ -47,6 +49,7 @@ def worker(rank, world, port, out, fused):
         assert r.fused == fused and not r.use_graph
         if fused:  # the 27 boxes split mid-layer: remote neighbours in x, y and z
             assert r.fh.remote
+            assert (r.fh.comm is not None) == slabs  # boundary / interior launches + side stream
         fin = r.advance(w.steps)
         got = fin.to_global().cpu().numpy()  # only this rank's boxes are non-zero
         c = p.coefficients()
@@ -66,18 +69,19 @@ def worker(rank, world, port, out, fused):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused", [False, True])
-def test_two_ranks_one_gpu_match_oracle(fused):
+@pytest.mark.parametrize("fused,slabs", [(False, False), (True, False), (True, True)])
+def test_two_ranks_one_gpu_match_oracle(fused, slabs):
     """fused=False: the overlapped unfused step; fused=True: the fused march
-    with the remote faces exchanged after each step."""
+    with the remote faces exchanged after each step (slabs: on a side stream,
+    overlapping the interior columns' launch)."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(worker, args=(2, free_port(), out, fused), nprocs=2, join=True)
+    mp.spawn(worker, args=(2, free_port(), out, fused, slabs), nprocs=2, join=True)
     for r in range(2):
         ok, sums_ok, max_ok, min_ok, n = out[r]
         assert ok, f"rank {r}: boxes differ from the oracle"
         assert sums_ok and max_ok and min_ok, f"rank {r}: reductions differ"
-    assert out[0][4] + out[1][4] == 27
+    assert out[0][4] + out[1][4] == (216 if slabs else 27)
 
 
 def nccl_world1_worker(rank, port, out):
