@@ -144,7 +144,11 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  * the fused FillBoundary of the next step.  Face halos only (7-point).
  * reverse != 0 (scatter mode only): every CTA walks its columns in reverse
  * order and marches z downward -- same results; a step that follows a
- * forward step then starts on the planes that step wrote last (L2-resident). */
+ * forward step then starts on the planes that step wrote last (L2-resident).
+ * Launched with programmatic stream serialization (PDL): the kernel's prologue
+ * may overlap the previous kernel on the stream; it waits (griddepcontrol.wait)
+ * for that kernel to complete before touching uold/unew, so stream order is
+ * preserved.  Environment TM_PDL=0 launches it as an ordinary kernel. */
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);
