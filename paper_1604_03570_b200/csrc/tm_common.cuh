@@ -123,6 +123,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// predicated 16-B global store (no branch around it)
+__device__ __forceinline__ void st_global_f64x2_if(uint64_t addr, double a, double b, bool pred) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "setp.ne.b32 P1, %3, 0;\n"
+        "@P1 st.global.v2.f64 [%0], {%1, %2};\n"
+        "}\n" ::"l"(addr),
+        "d"(a), "d"(b), "r"((int)pred)
+        : "memory");
+}
+
 // shared-window address forms (no generic->shared conversion in hot loops)
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");

@@ -236,6 +236,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         }
         const int64_t xstep = REV ? -2 * (int64_t)nyb : 2 * (int64_t)nyb;
         if (REV && xhp) xhp += (int64_t)(nk - 1) * 2 * nyb;  // x halo of the first plane processed
+        // RPW == 2: rows come in pairs (even column heights), so on[0] == on[1]
+        const bool xh_on = xhp != nullptr && on[0];
+        uint64_t xh_addr = reinterpret_cast<uint64_t>(xhp);
 
         // priming: planes k0-1 and k0 -> carried z flux and centre values
         double ua[RPW][CPL], ub[RPW][CPL], fzm[RPW][CPL];
@@ -346,7 +349,13 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                     for (int i = 0; i < RPW; ++i)
                         if (on[i]) st_cells(orow[i] + koff + zd, i);
                 }
-                if (xhp) {
+                if constexpr (RPW == 2) {
+                    // lanes 0 / 31 of the box's x faces: one predicated 16-B store of the warp's two
+                    // rows (consecutive y in the packed halo), no divergent branch in the plane loop
+                    st_global_f64x2_if(xh_addr, x_right ? out[0][CPL - 1] : out[0][0],
+                                       x_right ? out[1][CPL - 1] : out[1][0], xh_on);
+                    xh_addr += (uint64_t)(xstep * 8);
+                } else if (xhp) {
 #pragma unroll
                     for (int i = 0; i < RPW; ++i)
                         if (on[i]) xhp[i] = x_right ? out[i][CPL - 1] : out[i][0];
