@@ -31,6 +31,16 @@ namespace {
 
 using tmk::Segment;
 
+// TM_NBRH=0: fused steps scatter y/z faces into the ghosts of unew (the previous scheme)
+// instead of reading them from the neighbour boxes.
+bool nbr_halos_enabled() {
+    static const bool on = [] {
+        const char *v = getenv("TM_NBRH");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 // TMA ring depth (powers of two: stage and phase come from the plane counter by mask/shift).
 // (8 heat stages measured: C2 62.6 us vs 56.9 us at 4 -- fewer CTAs fit; C3/C5 within +-3 %.)
 #ifndef TM_HEAT_STAGES
@@ -80,15 +90,59 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
     }
 }
 
+// NBRH (fused mode, uniform columns): the z halo planes and the y halo rows at
+// box faces are read straight from the face neighbour's valid cells in uold
+// (the same values a FillBoundary would have copied into our ghosts), so the
+// step never writes y/z face ghosts of unew.  Faces whose neighbour is on
+// another rank (or none) still come from our own ghost cells, which the halo
+// exchange fills.  Stage rows: 0 = y0-1 (1-row box), 1..ny = the column
+// (ny-row box), ny+1 = y0+ny (1-row box); then the packed x halo.
+struct NbrFaces {
+    int32_t ylo, yhi, zlo, zhi;  // neighbour slot per face, < 0: use our own ghosts
+    bool top, bot;               // the column's first / last row is a box face
+};
+
+__device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensorMap *rmap, const CUtensorMap *xmap,
+                                          const MarchArgs &a, double *stage, uint64_t *bar, const tm_block &c,
+                                          const NbrFaces &f, int comp, int z, uint32_t tx_bytes) {
+    using namespace tmk;
+    const int nc = a.L.ncomp, g = a.L.nghost;
+    const int w = c.slot * nc + comp;
+    const int zl = z - g;  // valid z index of the plane
+    int ws = w, zs = z;
+    if (zl < 0 && f.zlo >= 0) {
+        ws = f.zlo * nc + comp;
+        zs = z + a.nzv;
+    } else if (zl >= a.nzv && f.zhi >= 0) {
+        ws = f.zhi * nc + comp;
+        zs = z - a.nzv;
+    }
+    const bool centre = zl >= 0 && zl < a.nzv;  // halo planes: only their column rows are used
+    mbar_arrive_expect_tx(bar, tx_bytes);
+    const int bx = a.box_x;
+    tma_load_plane(stage + bx, map, bar, c.x0, c.y0, zs, ws);
+    if (centre && f.top && f.ylo >= 0)
+        tma_load_plane(stage, rmap, bar, c.x0, c.y0 - 1 + a.nyv, zs, f.ylo * nc + comp);
+    else
+        tma_load_plane(stage, rmap, bar, c.x0, c.y0 - 1, zs, ws);
+    if (centre && f.bot && f.yhi >= 0)
+        tma_load_plane(stage + (c.ny + 1) * bx, rmap, bar, c.x0, c.y0 + c.ny - a.nyv, zs, f.yhi * nc + comp);
+    else
+        tma_load_plane(stage + (c.ny + 1) * bx, rmap, bar, c.x0, c.y0 + c.ny, zs, ws);
+    tma_load_plane(stage + a.xh_off, xmap, bar, c.y0 - g, 0, z - g, w);
+}
+
 // Warp-specialised pipeline: warps 0..NWARP-1 compute, warp NWARP is the TMA
 // producer.  full[s] completes when stage s holds its plane (TMA transaction
 // bytes); empty[s] completes when all NWARP consumer warps released it.  No
 // CTA-wide barrier in the steady state: fast warps run ahead up to the ring
 // depth while the producer refills each stage as soon as it is free.
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH>
 __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const __grid_constant__ CUtensorMap xmap,
+                                                                 const __grid_constant__ CUtensorMap rmap,
                                                                  MarchArgs a) {
+    static_assert(!NBRH || (PACKED && SCATTER), "neighbour-sourced halos belong to the fused mode");
     using namespace tmk;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
@@ -106,6 +160,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     if (tid == 0) {
         prefetch_tensormap(&map);
         if (PACKED) prefetch_tensormap(&xmap);
+        if (NBRH) prefetch_tensormap(&rmap);
 #pragma unroll
         for (int s = 0; s < kHeatStages; ++s) {
             mbar_init(&bars[s], 1);
@@ -124,11 +179,26 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 const Segment sg = a.segs[REV ? s_end - 1 - si : s_begin + si];
                 const tm_block c = a.cols[sg.col];
                 const int n = sg.k1 - sg.k0 + 2;
+                NbrFaces f{};
+                if (NBRH) {
+                    const int32_t *nb = a.nbr + 6 * c.slot;
+                    f.ylo = nb[2];
+                    f.yhi = nb[3];
+                    f.zlo = nb[4];
+                    f.zhi = nb[5];
+                    f.top = c.y0 - a.L.nghost == 0;
+                    f.bot = c.y0 - a.L.nghost + c.ny == a.nyv;
+                }
                 for (int q = 0; q < n; ++q, ++p) {
                     const int st_i = p % kHeatStages;
                     if (p >= kHeatStages) mbar_wait(&empty[st_i], ((p / kHeatStages) - 1) & 1);
-                    issue<PACKED>(&map, &xmap, a, stages + st_i * a.stage_elems, &bars[st_i], c, comp,
-                                  REV ? c.z0 + sg.k1 - q : c.z0 + sg.k0 - 1 + q, tx_bytes);
+                    const int z = REV ? c.z0 + sg.k1 - q : c.z0 + sg.k0 - 1 + q;
+                    if (NBRH)
+                        issue_nbr(&map, &rmap, &xmap, a, stages + st_i * a.stage_elems, &bars[st_i], c, f, comp, z,
+                                  tx_bytes);
+                    else
+                        issue<PACKED>(&map, &xmap, a, stages + st_i * a.stage_elems, &bars[st_i], c, comp, z,
+                                      tx_bytes);
                 }
             }
         }
@@ -207,12 +277,12 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         int kz_lo = -1, kz_hi = -1;
         int64_t zoff_lo = 0, zoff_hi = 0;
         if (SCATTER) {
-            if (warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
+            if (!NBRH && warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
                 ylo_i = 0;
                 ylo = orow[0] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
             }
             const int rl = c.ny - 1;  // last row of the column
-            if (yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
+            if (!NBRH && yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
                 yhi_i = rl % RPW;
                 yhi = obase + (int64_t)rl * st.row + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
             }
@@ -225,11 +295,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                       warp * RPW;
                 x_right = true;
             }
-            if (nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
+            if (!NBRH && nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
                 kz_lo = -zl0;
                 zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
             }
-            if (nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
+            if (!NBRH && nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
                 kz_hi = nzb - 1 - zl0;
                 zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
             }
@@ -336,14 +406,14 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 if (out[i][0] != 1234.5) continue;
 #endif
                 st_cells(orow[i] + koff, i);
-                if (SCATTER) {
+                if (SCATTER && !NBRH) {
                     if (i == ylo_i) st_cells(ylo + koff, i);
                     if (i == yhi_i) st_cells(yhi + koff, i);
                 }
             }
             if (SCATTER) {
                 const int kz = REV ? nk - 1 - kk : kk;  // plane index from k0
-                if (kz == kz_lo || kz == kz_hi) {  // warp-uniform, two planes per column
+                if (!NBRH && (kz == kz_lo || kz == kz_hi)) {  // warp-uniform, two planes per column
                     const int64_t zd = kz == kz_lo ? zoff_lo : zoff_hi;
 #pragma unroll
                     for (int i = 0; i < RPW; ++i)
@@ -643,10 +713,10 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 
 namespace {
 
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV>
-int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int nctas, int ncomp,
-                     size_t smem, cudaStream_t s) {
-    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV>;
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH>
+int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a,
+                     int nctas, int ncomp, size_t smem, cudaStream_t s) {
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -663,32 +733,32 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const Marc
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = tmk::pdl_enabled() ? 1 : 0;
-    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, xmap, a);
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, xmap, rmap, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march launch");
     return TM_OK;
 }
 
-template <bool PACKED, bool SCATTER, bool REV>
-int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const MarchArgs &a, int cpl, int rows, int nctas,
-                 int ncomp, size_t smem, cudaStream_t s) {
+template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false>
+int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a, int cpl,
+                 int rows, int nctas, int ncomp, size_t smem, cudaStream_t s) {
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
-        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
     if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp
-        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
-    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
-    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV>(map, xmap, a, nctas, ncomp, smem, s);
+    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
 }
 
 
@@ -791,6 +861,7 @@ int tm_march_plan_create(const tm_block *cols, int64_t ncols, int32_t nctas, tm_
     p->max_nx = mx;
     p->max_ny = my;
     p->even = even;
+    for (int64_t c = 0; c < ncols; ++c) p->uniform_ny = p->uniform_ny && cols[c].ny == my;
     cudaError_t e = cudaMalloc(&p->d_cols, sizeof(tm_block) * std::max<int64_t>(ncols, 1));
     if (e == cudaSuccess) e = cudaMalloc(&p->d_segs, sizeof(Segment) * std::max<size_t>(segs.size(), 1));
     if (e == cudaSuccess) e = cudaMalloc(&p->d_seg_begin, sizeof(int32_t) * (nctas + 1));
@@ -873,10 +944,24 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
     if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
     cudaStream_t s = as_stream(stream);
-    if (!packed) return launch_march<false, false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    if (!scatter) return launch_march<true, false, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    if (reverse) return launch_march<true, true, true>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    return launch_march<true, true, false>(map, xmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (!packed) return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    if (!scatter) return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    // neighbour-sourced y/z halos: the column rows and the two halo rows are separate boxes,
+    // each landing on a stage row that must be 128-B aligned (TMA destination)
+    if (p->uniform_ny && a.box_x % 16 == 0 && nbr_halos_enabled()) {
+        CUtensorMap cmap, rmap;
+        rc = encode_plane_map(&cmap, L, uold, a.box_x, p->max_ny);
+        if (rc) return rc;
+        rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
+        if (rc) return rc;
+        if (reverse)
+            return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+                                                        smem, s);
+        return launch_march<true, true, false, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+                                                     smem, s);
+    }
+    if (reverse) return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
 }
 
 int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,

@@ -22,4 +22,5 @@ struct tm_march_plan {
     int32_t *d_seg_begin = nullptr;
     int max_nx = 0, max_ny = 0;
     bool even = true;
+    bool uniform_ny = true;  // every column has max_ny rows
 };
