@@ -402,6 +402,10 @@ class FusedHalo:
                    id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
         table = face_neighbors(a, geom, multi)
         self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=a.device)
+        if max_rows is None and max(a.units[u].valid.extents[0] for u in a.local_units) > 64:
+            # 4 cells per lane: 32-row columns, one 17-warp CTA per SM (C3, 128-wide boxes: 1.71 ->
+            # 1.60 ms/step against 8-row columns at 2 CTAs/SM; tools/march_perf.py --config C3)
+            max_rows = 32
         self.plan = march_plan(a, True, max_rows, nctas)
         # Multi-rank: the columns of boxes with a face on another rank ("boundary" boxes) march
         # first; their faces travel on a side stream while the remaining columns march, so the
