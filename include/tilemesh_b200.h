@@ -51,7 +51,7 @@ extern "C" {
 #define TM_ERR_CUDA 2    /* CUDA runtime / driver failure */
 #define TM_ERR_NOMEM 3
 
-#define TM_ABI_VERSION 1
+#define TM_ABI_VERSION 2
 
 typedef struct tm_layout {
     int64_t nslots; /* FAB slots in the allocation */
@@ -135,41 +135,43 @@ int tm_residual_maxnorm(tm_sweep_plan *plan, const tm_layout *phi_layout, const 
 typedef struct tm_march_plan tm_march_plan;
 int tm_march_plan_create(const tm_block *columns, int64_t ncolumns, int32_t nctas, tm_march_plan **out);
 int tm_march_plan_destroy(tm_march_plan *plan);
-/* xh_old == NULL: x halos from the ghost columns of uold (FillBoundary must
- * have run).  xh_old != NULL: x halos from the packed buffer
- * xh[(slot*ncomp+c)][z][side][y] (valid y,z extents; side 0 = i = lo-1,
- * side 1 = i = hi+1).  xh_new != NULL additionally scatters every box's
- * boundary values into its face neighbours' halos in unew / xh_new
- * (d_nbr: 6 neighbour slots per slot, order -x,+x,-y,+y,-z,+z, -1 = none):
- * the fused FillBoundary of the next step.  Face halos only (7-point).
- * reverse != 0 (scatter mode only): every CTA walks its columns in reverse
- * order and marches z downward -- same results; a step that follows a
- * forward step then starts on the planes that step wrote last (L2-resident).
+/* Where a step's halos come from, and which halos of the new field it writes
+ * (halo_mode of tm_heat_march):
+ *   TM_HALO_GHOSTS        x/y/z halos from the ghost cells of uold (FillBoundary
+ *                         must have run); writes only valid cells of unew.
+ *                         xh_old, xh_new, d_nbr must be NULL, reverse 0.
+ *   TM_HALO_PACKED        x halos from the packed buffer xh_old
+ *                         xh[(slot*ncomp+c)][z][side][y] (valid y,z extents;
+ *                         side 0 = i = lo-1, side 1 = i = hi+1), y/z from the
+ *                         ghosts of uold; writes only valid cells of unew.
+ *   TM_HALO_FUSED_SCATTER as PACKED, and the epilogue also writes every box's
+ *                         boundary values into its face neighbours' halos of
+ *                         the new field: y/z ghost rows/planes of unew and the
+ *                         packed x halo xh_new (d_nbr: 6 neighbour slots per
+ *                         slot, order -x,+x,-y,+y,-z,+z; < 0 = none / remote).
+ *   TM_HALO_FUSED_NBR     y/z halos read straight from the face neighbours'
+ *                         valid cells in uold (own ghosts where d_nbr < 0),
+ *                         x halos from xh_old; the epilogue writes ONLY xh_new.
+ *                         The y/z face ghosts of unew are NOT written.  Needs
+ *                         columns of one height and width % 16 == 0.
+ * The fused modes are the FillBoundary of the next step fused into this one
+ * (face halos only: the 7-point stencil never reads edge/corner ghosts).  A
+ * SCATTER step must not follow an NBR step on the same packed halos (the y/z
+ * ghosts it reads were not written): the plan remembers the last fused mode
+ * and refuses that hand-over until tm_march_plan_reset_halos (call it after
+ * re-priming the halos with a FillBoundary).
+ * reverse != 0 (fused modes): every CTA walks its columns in reverse order and
+ * marches z downward -- same results; a step that follows a forward step then
+ * starts on the planes that step wrote last (L2-resident).
  * Launched with programmatic stream serialization (PDL): the kernel's prologue
  * may overlap the previous kernel on the stream; it waits (griddepcontrol.wait)
  * for that kernel to complete before touching uold/unew, so stream order is
- * preserved.  Environment TM_PDL=0 launches it as an ordinary kernel. */
+ * preserved. */
+enum { TM_HALO_GHOSTS = 0, TM_HALO_PACKED = 1, TM_HALO_FUSED_SCATTER = 2, TM_HALO_FUSED_NBR = 3 };
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
-                  int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
+                  int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);
-
-/* Two heat steps per launch (temporal blocking, Kernel A3): u2 = two
- * forward-Euler steps of u0 on every column of the plan, the intermediate
- * field computed in shared memory on the column plus a one-cell ring.
- * Bit-identical to two rounds of FillBoundary + tm_heat_sweep.  Columns:
- * even width <= 64, <= 16 rows; nghost >= 2.
- * xh_old == NULL: u0's two ghost layers are read from storage (FillBoundary
- * must have run); only valid cells of u2 are written.
- * xh_old != NULL: fused halo exchange for uniform boxes -- x halos from the
- * packed buffer xh[(slot*ncomp+c)][2*(z+2)+side][y+2][2] (side 0 = x -2,-1,
- * side 1 = x nx, nx+1; y in [-2, ny+1], z in [-2, nz+1]), y/z ghosts from
- * storage; every u2 cell within two layers of a box face is also written to
- * the neighbours' halos of the new field (storage y/z ghosts, xh_new): faces
- * two deep, edges one deep -- all the next launch reads.
- * d_nbr27[27*slot + (ox+1) + 3*(oy+1) + 9*(oz+1)] = neighbour slot, -1 = none. */
-int tm_heat_march2(tm_march_plan *plan, const tm_layout *layout, const double *u0, double *u2,
-                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD,
-                   const double *xh_old, double *xh_new, const int32_t *d_nbr27, void *stream);
+int tm_march_plan_reset_halos(tm_march_plan *plan);
 
 /* Fused red (0) / black (1) Gauss-Seidel pass of the column march, in place on
  * phi (ncomp 1), x halos from the packed buffer xh, and the updated colour's
@@ -200,7 +202,7 @@ int tm_gsrb_split_pass(tm_march_plan *plan, int32_t nslots, int32_t nx, int32_t 
 
 /* ---- 9-point 8th-order Laplacian step ("wide4", Kernel W) -------------------
  * Replaces compiled.wide4_tiles / wide4_range (compiled.py:102-141) as driven
- * by kernels.wide4_step (kernels.py:218-247) and loop_wide4_step
+ * by kernels.wide4_step (kernels.py:218-247) and the reference's loop variant
  * (kernels.py:309-342), over every column of a march plan (columns of the
  * full box width <= 128, <= 16 rows (<= 8 when wider than 64), full z).
  * coeffs5 = host array {c0, c1, c2, c3, c4} (StencilCoeffs8); dxi2_d = 1/dx_d^2;

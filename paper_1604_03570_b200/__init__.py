@@ -10,7 +10,6 @@ the GPU; every data-path operation is an sm_100a kernel of
 libtilemesh_b200.so (no CPU fallback).
 """
 
-from .arena import Arena, ArenaPool
 from .box import Box, box_diff, decompose, grow, intersect, shift, to_face
 from .boxarray import BoxArray, DistributionMapping, Geometry, partition
 from .configs import CONFIGS, Workload, make_init
@@ -34,21 +33,19 @@ from .stencil import (
     heat_amplification,
     heat_step,
     init_cosine,
-    loop_heat_step,
     residual_maxnorm,
 )
 from .wide4 import (
     StencilCoeffs8,
     Wide4Runner,
     derive_coeffs8,
-    loop_wide4_step,
     wide4_amplification,
     wide4_stable_dt,
     wide4_step,
 )
 
 __all__ = [
-    "Arena", "ArenaPool", "Box", "box_diff", "decompose", "grow", "intersect", "shift", "to_face",
+    "Box", "box_diff", "decompose", "grow", "intersect", "shift", "to_face",
     "BoxArray", "DistributionMapping", "Geometry", "partition",
     "CONFIGS", "Workload", "make_init", "FArrayBox", "copy_region", "intersect_copy",
     "CopyTag", "FillPlan", "build_fill_plan", "shift_candidates", "split_tags",
@@ -56,9 +53,8 @@ __all__ = [
     "CONTIGUOUS", "REGIONAL", "DeviceFab", "FillBoundary", "MultiFab", "fill_boundary",
     "read_plotfile", "write_plotfile",
     "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
-    "loop_heat_step",
     "residual_maxnorm",
-    "StencilCoeffs8", "Wide4Runner", "derive_coeffs8", "loop_wide4_step", "wide4_amplification", "wide4_stable_dt",
+    "StencilCoeffs8", "Wide4Runner", "derive_coeffs8", "wide4_amplification", "wide4_stable_dt",
     "wide4_step",
 ]
 

@@ -20,7 +20,10 @@ LIB_PATH = os.environ.get("TILEMESH_LIB") or os.path.join(HERE, "libtilemesh_b20
 TM_OK = 0
 TM_ERR_INVALID = 1
 TM_ERR_CUDA = 2
-ABI_VERSION = 1
+ABI_VERSION = 2
+
+# halo_mode of tm_heat_march (include/tilemesh_b200.h)
+HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR = 0, 1, 2, 3
 
 
 class tm_layout(ctypes.Structure):
@@ -45,9 +48,9 @@ EXPORTS = [
     "tm_copy_plan_create", "tm_copy_plan_destroy", "tm_copy_plan_elements", "tm_copy_run",
     "tm_sweep_plan_create", "tm_sweep_plan_destroy", "tm_heat_sweep", "tm_gsrb_color",
     "tm_residual_maxnorm", "tm_reduce_sum", "tm_reduce_minmax",
-    "tm_march_plan_create", "tm_march_plan_destroy", "tm_heat_march", "tm_gsrb_march", "tm_wide4_march",
+    "tm_march_plan_create", "tm_march_plan_destroy", "tm_march_plan_reset_halos", "tm_heat_march", "tm_gsrb_march", "tm_wide4_march",
     "tm_wide4_march_fused",
-    "tm_heat_march2", "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass",
+    "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass",
 ]
 
 _lib = None
@@ -86,11 +89,11 @@ def load():
     L.tm_reduce_minmax.argtypes = [vp, P(tm_layout), vp, i32, vp, vp]
     L.tm_march_plan_create.argtypes = [vp, i64, i32, P(vp)]
     L.tm_march_plan_destroy.argtypes = [vp]
-    L.tm_heat_march.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, i32, vp]
+    L.tm_march_plan_reset_halos.argtypes = [vp]
+    L.tm_heat_march.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, i32, vp, vp, vp, i32, vp]
     L.tm_gsrb_march.argtypes = [vp, P(tm_layout), vp, P(tm_layout), vp, i32, f64, vp, vp, vp]
     L.tm_wide4_march.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp]
     L.tm_wide4_march_fused.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp, vp, vp]
-    L.tm_heat_march2.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, vp]
     L.tm_gsrb_split.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, P(tm_layout), vp, vp, vp, vp]
     L.tm_gsrb_merge.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, vp]
     L.tm_gsrb_split_pass.argtypes = [vp, i32, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp]

@@ -20,15 +20,6 @@ int cuda_fail(cudaError_t e, const char *what);
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// Programmatic dependent launch for the step kernels (TM_PDL=0 turns it off).
-inline bool pdl_enabled() {
-    static const bool on = [] {
-        const char *v = getenv("TM_PDL");
-        return !(v && v[0] == '0');
-    }();
-    return on;
-}
-
 // element strides of a layout
 struct Strides {
     int64_t row, plane, comp, slot;

@@ -31,25 +31,9 @@ namespace {
 
 using tmk::Segment;
 
-// TM_NBRH=0: fused steps scatter y/z faces into the ghosts of unew (the previous scheme)
-// instead of reading them from the neighbour boxes.
-bool nbr_halos_enabled() {
-    static const bool on = [] {
-        const char *v = getenv("TM_NBRH");
-        return !(v && v[0] == '0');
-    }();
-    return on;
-}
-
 // TMA ring depth (powers of two: stage and phase come from the plane counter by mask/shift).
 // (8 heat stages measured: C2 62.6 us vs 56.9 us at 4 -- fewer CTAs fit; C3/C5 within +-3 %.)
-#ifndef TM_HEAT_STAGES
-#define TM_HEAT_STAGES 4
-#endif
-constexpr int kHeatStages = TM_HEAT_STAGES;
-#ifndef TM_MARCH_EXPERIMENT
-#define TM_MARCH_EXPERIMENT 0
-#endif
+constexpr int kHeatStages = 4;
 constexpr int kGsrbStages = 4;
 
 struct MarchArgs {
@@ -82,9 +66,7 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
         tma_load_plane(stage, map, bar, c.x0, c.y0 - 1, z, w);
         // x halo: y range of the column, both sides, valid plane z - nghost
         const int g = a.L.nghost;
-#if TM_MARCH_EXPERIMENT != 3  // 3: skip the x-halo copy (timing experiment; wrong results)
         tma_load_plane(stage + a.xh_off, xmap, bar, c.y0 - g, 0, z - g, w);
-#endif
     } else {
         tma_load_plane(stage, map, bar, (c.x0 - 1) & ~1, c.y0 - 1, z, w);
     }
@@ -155,7 +137,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int bx = a.box_x;
     const uint32_t tx_bytes =
-        (uint32_t)((a.box_x * a.box_y + (PACKED && TM_MARCH_EXPERIMENT != 3 ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
+        (uint32_t)((a.box_x * a.box_y + (PACKED ? 2 * (a.box_y - 2) : 0)) * (int)sizeof(double));
 
     if (tid == 0) {
         prefetch_tensormap(&map);
@@ -380,11 +362,7 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                     const double fzp = REV ? fzm[i][j] : fnew, fzn = REV ? fnew : fzm[i][j];
                     double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
                     sum = rn_add(sum, rn_mul(rn_sub(fzp, fzn), c2));
-#if TM_MARCH_EXPERIMENT == 1  // data movement only (timing experiments; wrong results)
-                    out[i][j] = u0;
-#else
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
-#endif
                     fzm[i][j] = fnew;
                 }
             }
@@ -402,9 +380,6 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 if (!on[i]) continue;
-#if TM_MARCH_EXPERIMENT == 2  // no stores (timing experiments; wrong results)
-                if (out[i][0] != 1234.5) continue;
-#endif
                 st_cells(orow[i] + koff, i);
                 if (SCATTER && !NBRH) {
                     if (i == ylo_i) st_cells(ylo + koff, i);
@@ -732,7 +707,7 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUte
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = tmk::pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = 1;
     cudaError_t e = cudaLaunchKernelEx(&cfg, kern, map, xmap, rmap, a);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "march launch");
@@ -892,9 +867,16 @@ int tm_march_plan_destroy(tm_march_plan *p) {
     return TM_OK;
 }
 
+int tm_march_plan_reset_halos(tm_march_plan *p) {
+    if (!p) return tmk::fail(TM_ERR_INVALID, "tm_march_plan_reset_halos: null plan");
+    p->last_halo_mode = -1;
+    p->last_xh_new = nullptr;
+    return TM_OK;
+}
+
 int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
-                  double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old, double *xh_new,
-                  const int32_t *d_nbr, int32_t reverse, void *stream) {
+                  double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode, const double *xh_old,
+                  double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream) {
     using namespace tmk;
     if (!p) return fail(TM_ERR_INVALID, "tm_heat_march: null plan");
     int rc = check_layout(layout, "tm_heat_march");
@@ -905,11 +887,41 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march: bad ncomp");
     if (strides_of(L).comp >= ((int64_t)1 << 32))
         return fail(TM_ERR_INVALID, "tm_heat_march: one component of a slot must hold < 2^32 doubles");
-    const bool packed = xh_old != nullptr;
-    const bool scatter = xh_new != nullptr;
-    if (scatter && (!packed || !d_nbr)) return fail(TM_ERR_INVALID, "tm_heat_march: scatter needs xh_old and nbr");
+    const bool packed = halo_mode != TM_HALO_GHOSTS;
+    const bool scatter = halo_mode == TM_HALO_FUSED_SCATTER || halo_mode == TM_HALO_FUSED_NBR;
+    switch (halo_mode) {
+        case TM_HALO_GHOSTS:
+            if (xh_old || xh_new || d_nbr || reverse)
+                return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_GHOSTS takes no halo buffers, table or reverse");
+            break;
+        case TM_HALO_PACKED:
+            if (!xh_old || xh_new || d_nbr || reverse)
+                return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_PACKED needs xh_old only");
+            break;
+        case TM_HALO_FUSED_SCATTER:
+        case TM_HALO_FUSED_NBR:
+            if (!xh_old || !xh_new || !d_nbr || xh_old == xh_new)
+                return fail(TM_ERR_INVALID, "tm_heat_march: fused modes need distinct xh_old / xh_new and d_nbr");
+            break;
+        default:
+            return fail(TM_ERR_INVALID, "tm_heat_march: unknown halo_mode " + std::to_string(halo_mode));
+    }
     if (p->ncols == 0) return TM_OK;
     if (!p->even) return fail(TM_ERR_INVALID, "tm_heat_march: columns must start on even x and have even width");
+    const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
+    if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
+    if (packed && p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_heat_march: packed x halo needs even column height");
+    // neighbour-sourced y/z halos: the column rows and the two halo rows are separate TMA boxes,
+    // each landing on a stage row that must be 128-B aligned (TMA destination)
+    if (halo_mode == TM_HALO_FUSED_NBR && !(p->uniform_ny && p->max_nx % 16 == 0))
+        return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_FUSED_NBR needs columns of one height and a width that "
+                                    "is a multiple of 16");
+    // A TM_HALO_FUSED_NBR step leaves the y/z face ghosts of unew unwritten; a following
+    // TM_HALO_FUSED_SCATTER step would read them.  Refuse that hand-over (tm_march_plan_reset_halos
+    // after a FillBoundary re-arms the plan).
+    if (halo_mode == TM_HALO_FUSED_SCATTER && p->last_halo_mode == TM_HALO_FUSED_NBR && xh_old == p->last_xh_new)
+        return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_FUSED_SCATTER after a TM_HALO_FUSED_NBR step reads y/z "
+                                    "ghosts that step did not write; FillBoundary + tm_march_plan_reset_halos first");
     MarchArgs a{};
     a.cols = p->d_cols;
     a.segs = p->d_segs;
@@ -935,33 +947,38 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     rc = encode_plane_map(&map, L, uold, a.box_x, a.box_y);
     if (rc) return rc;
     if (packed) {
-        if (p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_heat_march: packed x halo needs even column height");
         rc = encode_xh_map(&xmap, L, xh_old, p->max_ny);
         if (rc) return rc;
     } else {
         xmap = map;
     }
-    const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
-    if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
     cudaStream_t s = as_stream(stream);
-    if (!packed) return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    if (!scatter) return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    // neighbour-sourced y/z halos: the column rows and the two halo rows are separate boxes,
-    // each landing on a stage row that must be 128-B aligned (TMA destination)
-    if (p->uniform_ny && a.box_x % 16 == 0 && nbr_halos_enabled()) {
-        CUtensorMap cmap, rmap;
-        rc = encode_plane_map(&cmap, L, uold, a.box_x, p->max_ny);
-        if (rc) return rc;
-        rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
-        if (rc) return rc;
-        if (reverse)
-            return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
-                                                        smem, s);
-        return launch_march<true, true, false, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
-                                                     smem, s);
+    if (scatter) {
+        p->last_halo_mode = halo_mode;
+        p->last_xh_new = xh_new;
     }
-    if (reverse) return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-    return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    switch (halo_mode) {
+        case TM_HALO_GHOSTS:
+            return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+        case TM_HALO_PACKED:
+            return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+        case TM_HALO_FUSED_NBR: {
+            CUtensorMap cmap, rmap;
+            rc = encode_plane_map(&cmap, L, uold, a.box_x, p->max_ny);
+            if (rc) return rc;
+            rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
+            if (rc) return rc;
+            if (reverse)
+                return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+                                                            smem, s);
+            return launch_march<true, true, false, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+                                                         smem, s);
+        }
+        default:
+            if (reverse)
+                return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+            return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+    }
 }
 
 int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,

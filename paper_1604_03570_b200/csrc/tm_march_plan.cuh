@@ -23,4 +23,6 @@ struct tm_march_plan {
     int max_nx = 0, max_ny = 0;
     bool even = true;
     bool uniform_ny = true;  // every column has max_ny rows
+    int32_t last_halo_mode = -1;          // mode of the last fused tm_heat_march (tm_march_plan_reset_halos)
+    const void *last_xh_new = nullptr;    // and the packed x halo it wrote
 };

@@ -115,6 +115,8 @@ class HaloExchange:
         for ids in recvs.values():
             for n in ids:
                 self.remote_dst.setdefault(tags[n][0], []).append(tags[n][1])
+        # local units whose valid cells some other rank needs
+        self.send_units = sorted({tags[n][2] for ids in sends.values() for n in ids})
         pack_tags, self.send_spans, nsend = build(sends, True)
         unpack_tags, self.recv_spans, nrecv = build(recvs, False)
         self.pack = _native.CopyPlan(pack_tags, nc)

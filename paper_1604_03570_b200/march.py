@@ -18,8 +18,6 @@ Host side of ``csrc/tm_march.cu``:
 
 from __future__ import annotations
 
-import os
-
 import numpy as np
 
 from . import _native
@@ -28,7 +26,7 @@ from .boxarray import BoxIndex, Geometry
 from .multifab import MultiFab, cell_offsets
 
 SMEM_BUDGET = 220 * 1024
-STAGES = int(os.environ.get("TM_HEAT_STAGES", "4"))  # heat ring depth (tm_march.cu kHeatStages; same -D)
+STAGES = 4        # heat ring depth (tm_march.cu kHeatStages)
 GSRB_STAGES = 4   # GSRB ring depth (kGsrbStages)
 
 
@@ -73,10 +71,13 @@ def march_eligible(mf: MultiFab) -> bool:
     L = mf.layout
     if mf.nghost < 1 or not mf.local_units:
         return False
-    for u in mf.local_units:
-        e = mf.units[u].valid.extents
-        if e[0] % 2 or e[0] > 128:
-            return False
+    widths = [mf.units[u].valid.extents[0] for u in mf.local_units]
+    if any(nx % 2 or nx > 128 for nx in widths):
+        return False
+    # columns wider than 64 run 4 cells per lane: the widest must be a multiple of 4
+    # (tm_heat_march / tm_gsrb_march); other layouts take the tile kernel
+    if max(widths) > 64 and max(widths) % 4:
+        return False
     return L.xoff % 2 == 0
 
 
@@ -146,92 +147,16 @@ def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None 
     plan = march_plan(mf_old, False, max_rows, nctas)
     c = params.coefficients()
     _native.check(_native.load().tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
-                                               mf_old.ncomp, c[0], c[1], c[2], c[3], None, None, None, 0,
-                                               mf_old.stream()), "tm_heat_march")
+                                               mf_old.ncomp, c[0], c[1], c[2], c[3], _native.HALO_GHOSTS,
+                                               None, None, None, 0, mf_old.stream()), "tm_heat_march")
 
 
 # --------------------------------------------------------------------------
 # fused halo path
 # --------------------------------------------------------------------------
-def heat_march2(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None = None,
-                nctas: int | None = None, xh_old=None, xh_new=None, nbr27=None) -> None:
-    """Two heat steps in one launch (Kernel A3, tm_heat_march2): ``mf_new``
-    = two forward-Euler steps of ``mf_old``.  Without ``xh_old`` the 2+
-    ghost layers of ``mf_old`` must be filled; with packed x halos (see
-    ``FusedHalo2``) the launch also fills ``mf_new``'s halos.  Bit-identical to
-    FillBoundary + heat_step twice."""
-    if mf_old.nghost < 2:
-        raise ValueError("two-step march needs nghost >= 2")
-    if not mf_new.same_layout(mf_old):
-        raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
-    if not march_eligible(mf_old) or max(mf_old.units[u].valid.extents[0] for u in mf_old.local_units) > 64:
-        raise ValueError("two-step march needs boxes of even x extent <= 64")
-    plan = march_plan(mf_old, False, min(max_rows or 16, 16), nctas or sm_count(mf_old.device), tag="march2")
-    c = params.coefficients()
-
-    def ptr(t):
-        return None if t is None else t.data_ptr()
-
-    _native.check(_native.load().tm_heat_march2(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
-                                                mf_old.ncomp, c[0], c[1], c[2], c[3], ptr(xh_old), ptr(xh_new),
-                                                ptr(nbr27), mf_old.stream()), "tm_heat_march2")
-
-
-class FusedHalo2:
-    """Packed two-deep x halos + 27-neighbour table for a pair of nghost >= 2
-    MultiFabs stepped two steps per launch with the fused halo exchange."""
-
-    def __init__(self, a: MultiFab, b: MultiFab, geom: Geometry, nctas: int | None = None,
-                 max_rows: int | None = None, packed: bool = False):
-        import torch
-
-        if not (two_step_eligible(a, geom) and a.same_layout(b)) or a.nghost < 2:
-            raise ValueError("layout is not eligible for the two-step fused path")
-        self.geom = geom
-        L = a.layout
-        self.nyv = L.ny - 2 * L.nghost
-        self.nzv = L.nz - 2 * L.nghost
-        shape = (L.nslots * a.ncomp, 2 * (self.nzv + 4), self.nyv + 4, 2)
-        self.xh = {id(a): torch.zeros(shape, dtype=torch.float64, device=a.device),
-                   id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
-        self.nbr = torch.as_tensor(neighbors27(a, geom).reshape(-1), dtype=torch.int32, device=a.device)
-        self.nctas = nctas
-        self.max_rows = max_rows
-        self.packed = packed  # x halos in dense buffers (else storage ghost columns)
-        self._init = self._xh_init_plan(a)
-
-    def _xh_init_plan(self, mf: MultiFab):
-        """Copy tags: every slot's two x-halo sides <- its own ghost columns
-        (after a FillBoundary), rows [-2, ny+1], planes [-2, nz+1]."""
-        L = mf.layout
-        ng, ny4, nz4 = mf.nghost, self.nyv + 4, self.nzv + 4
-        tags = np.zeros(2 * L.nslots, dtype=_native.COPY_TAG_DTYPE)
-        for s, u in enumerate(mf.local_units):
-            nx = mf.units[u].valid.extents[0]
-            for side in (0, 1):
-                src = s * L.slot + (ng - 2) * L.plane + (ng - 2) * L.row + (L.xoff - 2 if side == 0 else L.xoff + nx)
-                dst = ((s * mf.ncomp) * 2 * nz4 + side) * ny4 * 2
-                tags[2 * s + side] = (dst, src, 2, ny4, nz4, 0)
-        self.xh_side = (2, 4 * ny4, 4 * ny4 * nz4)
-        return _native.CopyPlan(tags, mf.ncomp)
-
-    def prime(self, mf: MultiFab, plan=None) -> None:
-        """Fill every ghost of ``mf`` (FillBoundary) and its packed x halos."""
-        from .multifab import fill_boundary
-
-        fill_boundary(mf, self.geom, plan)
-        if self.packed:
-            self._init.run(self.xh[id(mf)].data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
-
-    def step2(self, new: MultiFab, old: MultiFab, params) -> None:
-        """Two fused steps: old -> new, halos of new filled for the next launch."""
-        if self.packed:
-            heat_march2(new, old, params, max_rows=self.max_rows, nctas=self.nctas, xh_old=self.xh[id(old)],
-                        xh_new=self.xh[id(new)], nbr27=self.nbr)
-        else:
-            heat_march2(new, old, params, max_rows=self.max_rows, nctas=self.nctas, nbr27=self.nbr)
-
-
+# --------------------------------------------------------------------------
+# fused halo path
+# --------------------------------------------------------------------------
 REMOTE = -2  # face_neighbors entry: the neighbour lives on another rank
 
 
@@ -284,63 +209,6 @@ def fusable(mf: MultiFab, geom: Geometry, allow_remote: bool = False) -> bool:
     if ny % 2 or (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
         return False
     return face_neighbors(mf, geom, allow_remote) is not None
-
-
-def neighbors27(mf: MultiFab, geom: Geometry):
-    """Per local slot, the slot of the box at every offset (ox, oy, oz) in
-    {-1,0,1}^3 (index (ox+1) + 3*(oy+1) + 9*(oz+1); the centre is the slot
-    itself), or None unless every such neighbour is one LOCAL box of
-    identical extents (uniform chopped domains, periodic or interior)."""
-    valids = [u.valid for u in mf.units]
-    index = BoxIndex(valids)
-    dom = geom.domain
-    n = dom.extents
-    table = np.full((len(mf.local_units), 27), -1, dtype=np.int32)
-    for s, u in enumerate(mf.local_units):
-        v = valids[u]
-        e = v.extents
-        for oz in (-1, 0, 1):
-            for oy in (-1, 0, 1):
-                for ox in (-1, 0, 1):
-                    o = (ox, oy, oz)
-                    img = []
-                    for d in range(3):
-                        lo = v.lo[d] + o[d] * e[d]
-                        if not (dom.lo[d] <= lo and lo + e[d] - 1 <= dom.hi[d]):
-                            if not geom.periodic[d]:
-                                return None
-                            lo = dom.lo[d] + (lo - dom.lo[d]) % n[d]
-                        img.append(lo)
-                    target = Box(img, [img[k] + e[k] - 1 for k in range(3)])
-                    hits = index.query(target)
-                    if len(hits) != 1 or valids[hits[0]] != target or hits[0] not in mf.slot_of:
-                        return None
-                    table[s, (ox + 1) + 3 * (oy + 1) + 9 * (oz + 1)] = mf.slot_of[hits[0]]
-    return table
-
-
-def two_step_eligible(mf: MultiFab, geom: Geometry) -> bool:
-    """Layouts the fused two-steps-per-launch path supports: uniform boxes of
-    width a multiple of 8 up to 64, y and z extents >= 4, every neighbour
-    (faces, edges, corners) a local box."""
-    if not mf.local_units or comm_info_world(mf) != 1:
-        return False
-    ext = {mf.units[u].valid.extents for u in mf.local_units}
-    if len(ext) != 1:
-        return False
-    (nx, ny, nz), = ext
-    if nx % 8 or nx > 64 or ny < 4 or nz < 4:
-        return False
-    L = mf.layout
-    if (L.ny - 2 * L.nghost) != ny or (L.nz - 2 * L.nghost) != nz:
-        return False
-    return neighbors27(mf, geom) is not None
-
-
-def comm_info_world(mf: MultiFab) -> int:
-    from .multifab import comm_info
-
-    return comm_info()[1]
 
 
 def xh_init_plan(mf: MultiFab, table, nyv: int, nzv: int):
@@ -407,6 +275,13 @@ class FusedHalo:
             # 1.60 ms/step against 8-row columns at 2 CTAs/SM; tools/march_perf.py --config C3)
             max_rows = 32
         self.plan = march_plan(a, True, max_rows, nctas)
+        # Halo mode (include/tilemesh_b200.h): with columns of one height and 128-B aligned
+        # rows the y/z halos are read from the neighbours' valid cells and the epilogue writes
+        # only the packed x halos (FUSED_NBR); otherwise it also scatters y/z face ghosts of
+        # the new field (FUSED_SCATTER).  Fixed for the lifetime of the pair.
+        cols = self.plan.columns
+        nbr_ok = len(set(cols["ny"].tolist())) == 1 and int(cols["nx"].max()) % 16 == 0
+        self.mode = _native.HALO_FUSED_NBR if nbr_ok else _native.HALO_FUSED_SCATTER
         # Multi-rank: the columns of boxes with a face on another rank ("boundary" boxes) march
         # first; their faces travel on a side stream while the remaining columns march, so the
         # NCCL exchange overlaps the interior sweep.  Each column is still
@@ -415,7 +290,17 @@ class FusedHalo:
         self.comm = None
         if multi:
             cols = self.plan.columns
-            bslots = np.nonzero((table == REMOTE).any(axis=1))[0]
+            # "boundary" slots: every slot whose cells travel to another rank (the source of
+            # any send tag -- faces, edges and corners), not only slots with a remote face:
+            # the exchange packs them on the comm stream while the interior columns march
+            from .multifab import _device_fill
+            from .fillplan import build_fill_plan as _bfp
+
+            fp = fill_plan = fill_plan if fill_plan is not None else _bfp(a, geom)
+            halo = _device_fill(a, fp)[1]
+            src_units = set(halo.send_units) if halo is not None else set()
+            bslots = np.array(sorted({a.slot_of[u] for u in src_units} |
+                                     set(np.nonzero((table == REMOTE).any(axis=1))[0].tolist())), dtype=np.int64)
             isb = np.isin(cols["slot"], bslots)
             if isb.any() and (~isb).any():
                 self.plan_b = _native.MarchPlan(cols[isb], self.plan.nctas)
@@ -447,6 +332,9 @@ class FusedHalo:
         fill_boundary(mf, self.geom, plan)
         xh = self.xh[id(mf)]
         self._init_plan.run(xh.data_ptr(), self.xh_side, mf.ptr, mf.layout.side(), mf.stream())
+        for p in (self.plan, self.plan_b, self.plan_i):
+            if p is not None:
+                _native.check(_native.load().tm_march_plan_reset_halos(p.handle), "tm_march_plan_reset_halos")
 
     def step(self, new: MultiFab, old: MultiFab, params, reverse: bool = False) -> None:
         """One fused step: sweep old -> new reading old's face halos and
@@ -460,7 +348,7 @@ class FusedHalo:
 
         def march(plan):
             _native.check(_native.load().tm_heat_march(
-                plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3],
+                plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3], self.mode,
                 self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
                 old.stream()), "tm_heat_march(fused)")
 

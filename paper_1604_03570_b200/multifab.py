@@ -27,6 +27,7 @@ import numpy as np
 from . import _native
 from .box import Box, check_tile_size, decompose, grow, split_extent
 from .boxarray import BoxArray, DistributionMapping, Geometry
+from .fab import BoxIndexed
 from .fillplan import FillPlan, build_fill_plan
 from .mfiter import TileSchedule, build_schedule
 
@@ -120,59 +121,30 @@ class Unit(NamedTuple):
     fab: "DeviceFab | None"  # None for units owned by another rank
 
 
-class DeviceFab:
+class DeviceFab(BoxIndexed):
     """One unit's FAB: a view of its slot in the MultiFab allocation.
 
     ``data`` is indexed like the reference's ``FArrayBox.data``:
-    ``data[i - lo0, j - lo1, k - lo2, c]`` over the allocation (grown) box.
+    ``data[i - lo0, j - lo1, k - lo2, c]`` over the allocation (grown) box
+    (a strided torch view, so writes land in the MultiFab).
     """
 
     def __init__(self, mf: "MultiFab", slot: int, abox: Box):
         self.abox = abox
         self.ncomp = mf.ncomp
         self.slot = slot
-        L = mf.layout
         nx, ny, nz = abox.extents
-        x0 = L.xoff - mf.nghost
-        blk = mf.data[slot, :, :nz, :ny, x0:x0 + nx]  # (c, z, y, x)
-        self.data = blk.permute(3, 2, 1, 0)  # (x, y, z, c)
-
-    def _check(self, i, j, k, c):
-        if not self.abox.contains_point((i, j, k)):
-            raise IndexError(f"index ({i},{j},{k}) outside {self.abox}")
-        if not 0 <= c < self.ncomp:
-            raise IndexError(f"component {c} out of range [0,{self.ncomp})")
+        x0 = mf.layout.xoff - mf.nghost
+        self.data = mf.data[slot, :, :nz, :ny, x0:x0 + nx].permute(3, 2, 1, 0)  # (x, y, z, c)
 
     def at(self, i: int, j: int, k: int, c: int = 0) -> float:
-        self._check(i, j, k, c)
-        lo = self.abox.lo
-        return float(self.data[i - lo[0], j - lo[1], k - lo[2], c].item())
+        return float(self.data[self._local(i, j, k, c)].item())
 
     def set_at(self, i: int, j: int, k: int, v: float, c: int = 0) -> None:
-        self._check(i, j, k, c)
-        lo = self.abox.lo
-        self.data[i - lo[0], j - lo[1], k - lo[2], c] = v
-
-    def view(self, region: Box, c0: int = 0, nc: int | None = None):
-        if not self.abox.contains(region):
-            raise ValueError(f"region {region} not contained in {self.abox}")
-        if nc is None:
-            nc = self.ncomp - c0
-        if c0 < 0 or c0 + nc > self.ncomp:
-            raise ValueError(f"components [{c0},{c0 + nc}) out of range")
-        lo = self.abox.lo
-        sl = tuple(slice(region.lo[d] - lo[d], region.hi[d] - lo[d] + 1) for d in range(3))
-        return self.data[sl + (slice(c0, c0 + nc),)]
-
-    def comp(self, c: int = 0):
-        return self.data[:, :, :, c]
+        self.data[self._local(i, j, k, c)] = v
 
     def fill(self, v: float, region: Box | None = None, c: int | None = None) -> None:
-        region = self.abox if region is None else region
-        if c is None:
-            self.view(region).fill_(v)
-        else:
-            self.view(region, c, 1).fill_(v)
+        self.view(self.abox if region is None else region, 0 if c is None else c, None if c is None else 1).fill_(v)
 
     def to_numpy(self) -> np.ndarray:
         """Host copy in the reference layout: (nx, ny, nz, ncomp), F-order."""
@@ -182,13 +154,6 @@ class DeviceFab:
     def flat(self) -> np.ndarray:
         """Host copy of the reference's flat storage (x fastest, component slowest)."""
         return self.to_numpy().ravel(order="F")
-
-    def offset(self, i: int, j: int, k: int, c: int = 0) -> int:
-        """Index of (i, j, k, c) in ``flat`` (reference fab.py:38-44)."""
-        self._check(i, j, k, c)
-        lo = self.abox.lo
-        nx, ny, nz = self.abox.extents
-        return (i - lo[0]) + nx * ((j - lo[1]) + ny * ((k - lo[2]) + nz * c))
 
 
 class MultiFab:

@@ -181,9 +181,15 @@ class HeatRunner:
             self._step(old, new)
             self.steps_done += 1
             k += 1
-        if self.fused and finalize:
-            fill_boundary(self.current, self.geom, self.plan)
+        if finalize:
+            self.finalize()
         return self.current
+
+    def finalize(self) -> None:
+        """Refresh every ghost of the current state (one FillBoundary; only the
+        fused path leaves edge/corner ghosts stale between steps)."""
+        if self.fused:
+            fill_boundary(self.current, self.geom, self.plan)
 
 
 def _nccl_world() -> bool:

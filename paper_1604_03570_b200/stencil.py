@@ -120,14 +120,6 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
                                   dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
 
 
-def loop_heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatParams, workers: int = 1,
-                   scratch: dict | None = None) -> None:
-    """The reference's loop-level threading baseline (kernels.py:250-305) is a
-    CPU variant of the same arithmetic; on the device it is ``heat_step``
-    (same bits).  ``scratch`` is accepted and left empty."""
-    heat_step(mf_new, mf_old, geom, params, None, workers)
-
-
 def heat_sweep_plan(mf_new: MultiFab, mf_old: MultiFab, params: HeatParams, plan) -> None:
     """Kernel A over an explicit block table (e.g. the interior or boundary
     half of an overlapped step).  No checks: internal helper."""
@@ -265,7 +257,9 @@ def gsrb_solve(phi: MultiFab, rhs: MultiFab, geom: Geometry, sweeps: int, schedu
     from .multifab import comm_info
 
     _check_poisson(phi, rhs)
-    route_key = ("gsrb_route", geom, id(rhs), rhs.layout, comm_info()[1])
+    # caches key on the rhs LAYOUT, not its identity: a caller that builds a new rhs per solve
+    # (multigrid, time loops) reuses one solver object, rebound to the new rhs below
+    route_key = ("gsrb_route", geom, rhs.layout, tuple(rhs.local_units), comm_info()[1])
     route = phi._plans.get(route_key)
     if route is None:  # layout checks cost host time: once per (phi, rhs, geometry)
         can_ = comm_info()[1] == 1 and fusable(phi, geom)
@@ -276,11 +270,14 @@ def gsrb_solve(phi: MultiFab, rhs: MultiFab, geom: Geometry, sweeps: int, schedu
         raise ValueError("fused GSRB needs one rank and a uniform fully-covered box layout")
     if (can if fused is None else fused):
         use_split = split_ok if split is None else split
-        key = ("fused_gsrb", id(rhs), max_rows, use_split)
+        key = ("fused_gsrb", geom, rhs.layout, tuple(rhs.local_units), max_rows, use_split)
         fg = phi._plans.get(key)
         if fg is None:
             fg = (SplitGSRB if use_split else FusedGSRB)(phi, rhs, geom, max_rows)
             phi._plans[key] = fg
+        elif fg.rhs is not rhs:  # same layout, new array: rebind (the captured graph holds rhs pointers)
+            fg.rhs = rhs
+            fg._graph = None
         fg.prime(plan)
         fg.run(sweeps)
         fg.finalize(plan)

@@ -1,7 +1,7 @@
 """The 9-point 8th-order Laplacian step ("wide4").
 
 Reference: ``StencilCoeffs8`` / ``derive_coeffs8`` (kernels.py:49-83),
-``wide4_step`` (kernels.py:218-247), ``loop_wide4_step`` (kernels.py:309-342),
+``wide4_step`` (kernels.py:218-247),
 ``wide4_amplification`` / ``wide4_stable_dt`` (kernels.py:380-404), cell form
 ``compiled.wide4_range`` (compiled.py:102-129).
 
@@ -140,15 +140,6 @@ def wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: 
     ``workers`` are accepted for API parity (the result does not depend on
     the tiling, reference test_kernels.py:360-368): the device
     decomposition is the persistent column march."""
-    _check(mf_new, mf_old)
-    _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)
-
-
-def loop_wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: float, dt: float,
-                    workers: int = 1, coeffs: StencilCoeffs8 | None = None) -> None:
-    """The reference's loop-level baseline (z loop split over threads) is a
-    CPU threading variant of the same arithmetic; on the device it is the
-    same kernel."""
     _check(mf_new, mf_old)
     _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)
 

@@ -69,25 +69,3 @@ def test_farraybox_api():
         copy_region(fab, Box((1, 2, 3), (2, 2, 3)), other, Box((3, 3, 3), (3, 3, 3)))
 
 
-def test_arena_pool_semantics():
-    """Host scratch arenas keep the reference's contract (iterator.py:193-266):
-    grow-only, live until reset, one owner thread, high-water in bytes."""
-    import threading
-
-    from paper_1604_03570_b200 import ArenaPool
-
-    pool = ArenaPool(2)
-    a = pool.arenas[0].acquire_f64((3, 4))
-    a[...] = 1.0
-    b = pool.acquire(0, 20)  # 3 doubles
-    assert a.shape == (3, 4) and b.size == 3 and np.all(a == 1.0)
-    assert pool.high_water_bytes() == 8 * 15
-    pool.reset(0)
-    pool.acquire(0, 8)
-    assert pool.high_water_bytes() == 8 * 15
-    err = []
-    t = threading.Thread(target=lambda: err.append(pytest.raises(RuntimeError, pool.acquire, 0, 8)))
-    t.start()
-    t.join()
-    assert err
-    pool.release_owners()

@@ -159,57 +159,6 @@ def test_fused_reverse_direction_matches_oracle(tm, cfg, n, mgs, steps, rows, nc
     assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
 
 
-@pytest.mark.parametrize("cfg,n,mgs,steps,nctas", [
-    ("C2", 64, 32, 2, None),
-    ("C2", 64, 32, 4, 7),      # segments crossing columns
-    ("C2", 96, 48, 2, None),   # 48-wide boxes: idle lanes, 16-row columns of 48-row boxes
-    ("C5", 64, 32, 2, 5),      # 2 components, 32-wide (1 cell per lane)
-    ("C1", 40, 20, 2, None),   # 20-wide boxes, columns of 16 + 4 rows
-])
-def test_two_step_march_matches_oracle(tm, cfg, n, mgs, steps, nctas):
-    import dataclasses
-
-    from paper_1604_03570_b200.march import heat_march2
-
-    w = dataclasses.replace(tm.CONFIGS[cfg].scaled(n, mgs, steps), nghost=2)
-    geom, ba, glob, a = setup(tm, w)
-    b = a.clone_empty()
-    p = tm.HeatParams.stable(1.0, geom.dx)
-    plan = tm.build_fill_plan(a, geom)
-    for _ in range(steps // 2):
-        tm.fill_boundary(a, geom, plan)
-        heat_march2(b, a, p, nctas=nctas)
-        a, b = b, a
-    assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
-
-
-@pytest.mark.parametrize("packed", [False, True])
-@pytest.mark.parametrize("cfg,n,mgs,steps,nctas,rows", [
-    ("C2", 64, 32, 6, None, None),
-    ("C2", 64, 16, 4, 7, None),     # 16-wide boxes, segments crossing columns
-    ("C5", 64, 32, 4, None, 8),     # 2 components, 8-row columns
-    ("C1", 48, 24, 4, 5, None),     # 24-wide boxes: columns of 16 + 8 rows
-    ("C1", 32, 8, 4, 40, 8),        # 8-wide boxes: one lane feeds both x sides
-])
-def test_two_step_scatter_matches_oracle(tm, cfg, n, mgs, steps, nctas, rows, packed):
-    """Consecutive two-step launches with the fused ghost scatter (no
-    FillBoundary in between) give the oracle's bits."""
-    import dataclasses
-
-    from paper_1604_03570_b200.march import FusedHalo2
-
-    w = dataclasses.replace(tm.CONFIGS[cfg].scaled(n, mgs, steps), nghost=2)
-    geom, ba, glob, a = setup(tm, w)
-    b = a.clone_empty()
-    p = tm.HeatParams.stable(1.0, geom.dx)
-    fh = FusedHalo2(a, b, geom, nctas, rows, packed)
-    fh.prime(a)
-    for _ in range(steps // 2):
-        fh.step2(b, a, p)
-        a, b = b, a
-    assert np.array_equal(a.to_global().cpu().numpy(), oracle_steps(tm, w, glob, steps))
-
-
 @pytest.mark.parametrize("n,mgs,sweeps,rows", [(64, 32, 5, None), (64, 32, 4, 8), (32, 16, 6, None),
                                                (128, 64, 3, None), (48, 24, 3, 8), (128, 128, 2, None),
                                                (64, 64, 2, 12)])

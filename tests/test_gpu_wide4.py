@@ -152,13 +152,13 @@ def test_wide4_order_at_least_7_5(tm):
     assert math.log2(err(16) / err(32)) >= 7.5
 
 
-def test_wide4_tiling_and_loop_variant_bitwise(tm):
+def test_wide4_tiling_and_workers_bitwise(tm):
     w = dataclasses.replace(tm.CONFIGS["C1"].scaled(32, 16, 2), nghost=4)
     glob = tm.make_init(w)
     geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
     dt = tm.wide4_stable_dt(1.0, geom.dx)
     outs = []
-    for variant in ("tiled", "loop"):
+    for variant in ("tiled", "untiled"):
         mf = tm.MultiFab(tm.BoxArray.chop(w.domain, 16), 1, 4)
         mf.from_global(glob)
         out = mf.clone_empty()
@@ -167,7 +167,7 @@ def test_wide4_tiling_and_loop_variant_bitwise(tm):
             if variant == "tiled":
                 tm.wide4_step(out, mf, geom, 1.0, dt, tm.build_schedule(mf, (8, 4, 4)), workers=3)
             else:
-                tm.loop_wide4_step(out, mf, geom, 1.0, dt, workers=2)
+                tm.wide4_step(out, mf, geom, 1.0, dt, None, workers=2)
             mf, out = out, mf
         outs.append(mf.to_global().cpu().numpy())
     assert np.array_equal(outs[0], outs[1])

@@ -73,7 +73,8 @@ def packed_noscatter(cfg="C2", rows=16, nctas=296):
 
     def go():
         _native.check(_native.load().tm_heat_march(fh.plan.handle, a.layout.to_c(), a.ptr, b.ptr, a.ncomp, c[0], c[1],
-                                                   c[2], c[3], fh.xh[id(a)].data_ptr(), None, None, 0, a.stream()), "m")
+                                                   c[2], c[3], _native.HALO_PACKED, fh.xh[id(a)].data_ptr(), None, None, 0,
+                                                   a.stream()), "m")
     ms = graph_time(go, 20)
     print(f"{cfg} packed-noscatter rows={rows} nctas={nctas}: {ms * 1e3:.1f} us")
 
