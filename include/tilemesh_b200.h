@@ -51,7 +51,7 @@ extern "C" {
 #define TM_ERR_CUDA 2    /* CUDA runtime / driver failure */
 #define TM_ERR_NOMEM 3
 
-#define TM_ABI_VERSION 2
+#define TM_ABI_VERSION 3
 
 typedef struct tm_layout {
     int64_t nslots; /* FAB slots in the allocation */
@@ -233,6 +233,32 @@ int tm_reduce_sum(tm_sweep_plan *plan, const tm_layout *layout, const double *ba
 /* d_out[0] = max, d_out[1] = min over block cells of component comp. */
 int tm_reduce_minmax(tm_sweep_plan *plan, const tm_layout *layout, const double *base, int32_t comp,
                      double *d_out, void *stream);
+
+/* ---- inter-GPU halo exchange (NCCL) ----------------------------------------
+ * Replaces the remote half of fill_boundary (level.py:297-323) when boxes live
+ * on several GPUs (one process per GPU): pack the outgoing
+ * ghost data with tm_copy_run (packed side), move every message of the fill
+ * with ONE grouped ncclSend/ncclRecv to the neighbour ranks only, unpack with
+ * tm_copy_run.  BoxLib's aggregated remote-ghost buffers: PAPER.md:303-314.
+ * NCCL is dlopen'ed (an already loaded libnccl.so.2 is reused; TM_NCCL_LIB
+ * overrides the path).  tm_comm_create binds to the current CUDA device; the
+ * caller shares the 128-byte unique id of rank 0 (e.g. through the
+ * torch.distributed store) at setup only.  tm_halo_exchange is asynchronous
+ * on `stream` and may be captured into a CUDA graph. */
+typedef struct tm_comm tm_comm;
+typedef struct tm_exchange tm_exchange;
+int tm_comm_nccl_version(int32_t *version);
+int tm_comm_unique_id(uint8_t *out128);
+int tm_comm_create(const uint8_t *id128, int32_t nranks, int32_t rank, tm_comm **out);
+int tm_comm_destroy(tm_comm *comm);
+/* npeers distinct ascending peer ranks; message i: send_count[i] doubles at
+ * sendbuf + send_off[i] to peers[i], recv_count[i] doubles from peers[i] into
+ * recvbuf + recv_off[i] (counts may be 0 on either side). */
+int tm_exchange_create(tm_comm *comm, int32_t npeers, const int32_t *peers, const int64_t *send_off,
+                       const int64_t *send_count, const int64_t *recv_off, const int64_t *recv_count,
+                       tm_exchange **out);
+int tm_exchange_destroy(tm_exchange *x);
+int tm_halo_exchange(tm_exchange *x, const double *sendbuf, double *recvbuf, void *stream);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",  # belt and braces: the stencil arithmetic must stay FMA-free
     "-Xcompiler", "-fPIC", "-shared",
+    "-ldl",  # NCCL is dlopen'ed (csrc/tm_comm.cu)
 ]
 
 

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("TILEMESH_LIB") or os.path.join(HERE, "libtilemesh_b20
 TM_OK = 0
 TM_ERR_INVALID = 1
 TM_ERR_CUDA = 2
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 # halo_mode of tm_heat_march (include/tilemesh_b200.h)
 HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR = 0, 1, 2, 3
@@ -51,6 +51,8 @@ EXPORTS = [
     "tm_march_plan_create", "tm_march_plan_destroy", "tm_march_plan_reset_halos", "tm_heat_march", "tm_gsrb_march", "tm_wide4_march",
     "tm_wide4_march_fused",
     "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass",
+    "tm_comm_nccl_version", "tm_comm_unique_id", "tm_comm_create", "tm_comm_destroy",
+    "tm_exchange_create", "tm_exchange_destroy", "tm_halo_exchange",
 ]
 
 _lib = None
@@ -68,6 +70,10 @@ def load():
     if not os.path.exists(LIB_PATH):
         raise TilemeshError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                             "g.build()'` (nvcc, sm_100a); there is no CPU fallback")
+    try:  # torch loads its libnccl.so.2 at import: tm_comm.cu then reuses it (one NCCL per process)
+        import torch  # noqa: F401
+    except ImportError:  # pragma: no cover
+        pass
     L = ctypes.CDLL(LIB_PATH)
     vp, i32, i64, f64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
     P = ctypes.POINTER
@@ -97,6 +103,13 @@ def load():
     L.tm_gsrb_split.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, P(tm_layout), vp, vp, vp, vp]
     L.tm_gsrb_merge.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, vp]
     L.tm_gsrb_split_pass.argtypes = [vp, i32, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp]
+    L.tm_comm_nccl_version.argtypes = [P(i32)]
+    L.tm_comm_unique_id.argtypes = [ctypes.c_char_p]
+    L.tm_comm_create.argtypes = [ctypes.c_char_p, i32, i32, P(vp)]
+    L.tm_comm_destroy.argtypes = [vp]
+    L.tm_exchange_create.argtypes = [vp, i32, vp, vp, vp, vp, vp, P(vp)]
+    L.tm_exchange_destroy.argtypes = [vp]
+    L.tm_halo_exchange.argtypes = [vp, vp, vp, vp]
     for name in EXPORTS:
         if name not in ("tm_last_error", "tm_abi_version", "tm_copy_plan_elements"):
             getattr(L, name).restype = ctypes.c_int

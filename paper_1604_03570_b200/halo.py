@@ -12,12 +12,15 @@ exchange:
   packed x-fastest then y, z, component (``tm_side`` "packed" format);
 * rank a packs all its outgoing messages with one copy-kernel launch into
   one send buffer (messages in ascending peer order), every message of the
-  exchange travels in ONE ``torch.distributed.all_to_all_single`` call with
-  per-peer split sizes (NCCL: one grouped send/recv; zero-sized splits for
-  ranks that are not neighbours), and rank b unpacks all its incoming
-  messages with one launch straight into ghost cells.  One host call per
-  exchange keeps the issue cost low, and the collective is capturable in a
-  CUDA graph (``runner.HeatRunner`` replays multi-rank steps).
+  exchange travels in ONE grouped ``ncclSend`` / ``ncclRecv`` with the
+  neighbour ranks only (``tm_halo_exchange`` in the C-ABI, on the library's
+  own communicator: torch.distributed only carries the unique id at setup),
+  and rank b unpacks all its incoming messages with one launch straight
+  into ghost cells.  One host call per exchange keeps the issue cost low,
+  and the exchange is capturable in a CUDA graph (``runner.HeatRunner``
+  replays multi-rank steps).  Under the gloo backend (CPU tests, several
+  ranks sharing one GPU) the messages go through a host-staged
+  ``all_to_all_single`` with per-peer split sizes instead.
 
 Intra-rank tags never touch a buffer: they are the local copy kernel.
 """
@@ -130,33 +133,129 @@ class HaloExchange:
         self.recv_splits = split_sizes(self.recv_spans, mf.dm.nranks)
         self._work = None
         self._host = None
+        self._side = None  # NCCL: pack + send/recv run on this stream
+        self._x = None     # NCCL: tm_exchange handle
 
     def start(self, mf, stream: int) -> None:
         """Pack every outgoing message of ``mf`` (one launch) and post the
-        exchange (one all-to-all with per-peer splits).  NCCL orders it after
-        the pack on the current stream; ``finish`` makes the stream wait for
-        it and unpacks.  The exchange object is shared by every MultiFab of
-        the same layout (e.g. both buffers of a double-buffered pair), so the
-        field is passed per call."""
+        exchange.  Over NCCL both go on this exchange's side stream (forked
+        from the current stream), so work the caller queues next overlaps the
+        transfer; ``finish`` joins the side stream and unpacks.  The exchange
+        object is shared by every MultiFab of the same layout (e.g. both
+        buffers of a double-buffered pair), so the field is passed per call."""
         import torch
-        import torch.distributed as dist
 
-        self.pack.run(self.sendbuf.data_ptr(), (0, 0, 0), mf.ptr, mf.layout.side(), stream)
         if self._host is None:
+            import torch.distributed as dist
+
             self._host = dist.get_backend() == "gloo"
-        if self._host:  # CPU transport (tests): stage through host memory
+        if self._host:  # CPU transport (tests): stage through host memory, torch all-to-all
+            import torch.distributed as dist
+
+            self.pack.run(self.sendbuf.data_ptr(), (0, 0, 0), mf.ptr, mf.layout.side(), stream)
             torch.cuda.current_stream(self.device).synchronize()
             sbuf = self.sendbuf[:self.nsend].cpu()
             self._hrecv = torch.empty(self.nrecv, dtype=torch.float64)
-        else:
-            sbuf, self._hrecv = self.sendbuf[:self.nsend], self.recvbuf[:self.nrecv]
-        self._work = dist.all_to_all_single(self._hrecv, sbuf, self.recv_splits, self.send_splits,
-                                            async_op=True)
+            self._work = dist.all_to_all_single(self._hrecv, sbuf, self.recv_splits, self.send_splits,
+                                                async_op=True)
+            return
+        x = self._nccl_exchange()
+        cur = torch.cuda.current_stream(self.device)
+        if self._side is None:
+            self._side = torch.cuda.Stream(self.device)
+        self._side.wait_stream(cur)
+        side = self._side.cuda_stream
+        self.pack.run(self.sendbuf.data_ptr(), (0, 0, 0), mf.ptr, mf.layout.side(), side)
+        _native.check(_native.load().tm_halo_exchange(x, self.sendbuf.data_ptr(), self.recvbuf.data_ptr(), side),
+                      "tm_halo_exchange")
 
     def finish(self, mf, stream: int) -> None:
-        if self._work is not None:
-            self._work.wait()
-        self._work = None
+        import torch
+
         if self._host:
+            if self._work is not None:
+                self._work.wait()
+            self._work = None
             self.recvbuf[:self.nrecv].copy_(self._hrecv)
+        else:
+            torch.cuda.current_stream(self.device).wait_stream(self._side)
         self.unpack.run(mf.ptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)
+
+    def _nccl_exchange(self):
+        """The library-side plan of this exchange's messages (``tm_exchange``:
+        neighbour ranks only, offsets into the send / receive buffers)."""
+        if self._x is None:
+            import ctypes
+
+            peers = sorted({p for p, _, n in self.send_spans if n} | {p for p, _, n in self.recv_spans if n})
+            send = {p: (o, n) for p, o, n in self.send_spans}
+            recv = {p: (o, n) for p, o, n in self.recv_spans}
+            arr = lambda v, t: np.ascontiguousarray(np.array(v, dtype=t).reshape(-1))  # noqa: E731
+            pe = arr(peers, np.int32)
+            so = arr([send.get(p, (0, 0))[0] for p in peers], np.int64)
+            sc = arr([send.get(p, (0, 0))[1] for p in peers], np.int64)
+            ro = arr([recv.get(p, (0, 0))[0] for p in peers], np.int64)
+            rc = arr([recv.get(p, (0, 0))[1] for p in peers], np.int64)
+            h = ctypes.c_void_p()
+            ptr = lambda a: a.ctypes.data if len(a) else None  # noqa: E731
+            _native.check(_native.load().tm_exchange_create(nccl_comm().handle, len(peers), ptr(pe), ptr(so),
+                                                            ptr(sc), ptr(ro), ptr(rc), ctypes.byref(h)),
+                          "tm_exchange_create")
+            self._x = h
+            self._keep = (pe, so, sc, ro, rc)
+            self.peers = peers
+        return self._x
+
+    def __del__(self):
+        x = getattr(self, "_x", None)
+        if x is not None and _native._lib is not None:
+            _native._lib.tm_exchange_destroy(x)
+            self._x = None
+
+
+class NcclComm:
+    """The process's NCCL communicator for halo traffic (``tm_comm``), built
+    once over the default torch.distributed group: rank 0's unique id is
+    broadcast through torch.distributed at setup only; every message after
+    that goes through the library (``tm_halo_exchange``)."""
+
+    def __init__(self):
+        import ctypes
+
+        import torch.distributed as dist
+
+        L = _native.load()
+        rank, world = dist.get_rank(), dist.get_world_size()
+        uid = ctypes.create_string_buffer(128)
+        if rank == 0:
+            _native.check(L.tm_comm_unique_id(uid), "tm_comm_unique_id")
+        box = [uid.raw if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0)
+        h = ctypes.c_void_p()
+        _native.check(L.tm_comm_create(box[0], world, rank, ctypes.byref(h)), "tm_comm_create")
+        self.handle = h
+        self.rank, self.world = rank, world
+
+    def close(self) -> None:
+        if self.handle is not None and _native._lib is not None:
+            _native._lib.tm_comm_destroy(self.handle)
+        self.handle = None
+
+
+_COMM = None
+
+
+def nccl_comm() -> NcclComm:
+    global _COMM
+    if _COMM is None:
+        _COMM = NcclComm()
+    return _COMM
+
+
+def close_comm() -> None:
+    """Destroy the halo communicator (before ``destroy_process_group``; any
+    graph holding its work must be released first)."""
+    global _COMM
+    if _COMM is not None:
+        _COMM.close()
+        _COMM = None

@@ -1,6 +1,7 @@
 """The multi-rank device path end to end on ONE GPU: two processes share
-cuda:0 and exchange halos through torch.distributed (gloo, host-staged; the
-bench uses NCCL over NVLink with the same pack / send-recv / unpack code).
+cuda:0 and exchange halos through torch.distributed (gloo, host-staged; with
+NCCL the same pack / unpack kernels run around the library's grouped
+ncclSend/ncclRecv, tm_halo_exchange, tested here on a one-rank loopback).
 No kernel waits on another process, so sharing the device is safe.  Checks
 the overlapped step (interior sweep while messages are in flight), the fused
 march with its cross-rank face exchange, the multi-rank checksum protocol and
@@ -85,12 +86,17 @@ def test_two_ranks_one_gpu_match_oracle(fused, slabs):
 
 
 def nccl_world1_worker(rank, port, out):
-    """One NCCL rank: (1) the halo all-to-all (per-peer splits) captured in
-    a CUDA graph replays correctly; (2) the runner's verified-capture
-    bookkeeping (capture pair + eager check pair) lands on the right step."""
+    """One NCCL rank: (1) the library's own communicator (tm_comm_create from
+    a unique id broadcast over torch.distributed) moves a halo message to
+    itself with tm_halo_exchange (grouped ncclSend/ncclRecv), eagerly and
+    captured in a CUDA graph; (2) the runner's verified-capture bookkeeping
+    (capture pair + eager check pair) lands on the right step."""
+    import ctypes
+
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
+    from paper_1604_03570_b200 import _native, halo
     from paper_1604_03570_b200.runner import HeatRunner
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -98,22 +104,37 @@ def nccl_world1_worker(rank, port, out):
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
     try:
+        L = _native.load()
+        comm = halo.nccl_comm()
+        ver = ctypes.c_int32()
+        _native.check(L.tm_comm_nccl_version(ctypes.byref(ver)), "version")
+        # one "peer" (ourselves): 600 doubles out of sendbuf+100 into recvbuf+50
+        pe = np.array([0], np.int32)
+        so, sc, ro, rc = (np.array([v], np.int64) for v in (100, 600, 50, 600))
+        x = ctypes.c_void_p()
+        _native.check(L.tm_exchange_create(comm.handle, 1, pe.ctypes.data, so.ctypes.data, sc.ctypes.data,
+                                           ro.ctypes.data, rc.ctypes.data, ctypes.byref(x)), "create")
         src = torch.arange(1000, dtype=torch.float64, device="cuda")
-        dst = torch.zeros(600, dtype=torch.float64, device="cuda")
-        dist.all_to_all_single(dst, src[:600], [600], [600])  # eager warm-up
+        dst = torch.zeros(700, dtype=torch.float64, device="cuda")
+        st = torch.cuda.current_stream().cuda_stream
+        _native.check(L.tm_halo_exchange(x, src.data_ptr(), dst.data_ptr(), st), "eager")
         torch.cuda.synchronize()
+        eager_ok = bool(torch.equal(dst[50:650], src[100:700])) and not bool(dst[:50].any())
         dst.zero_()
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s), torch.cuda.graph(g, stream=s):
-            w = dist.all_to_all_single(dst, src[:600] * 2, [600], [600], async_op=True)
-            w.wait()
+            src.mul_(2.0)
+            _native.check(L.tm_halo_exchange(x, src.data_ptr(), dst.data_ptr(), s.cuda_stream), "captured")
         torch.cuda.current_stream().wait_stream(s)
         g.replay()
         torch.cuda.synchronize()
-        a2a_ok = bool(torch.equal(dst, src[:600] * 2))
-        del g  # a live graph holding NCCL work blocks destroy_process_group
+        a2a_ok = eager_ok and bool(torch.equal(dst[50:650], 2.0 * torch.arange(100, 700, dtype=torch.float64,
+                                                                               device="cuda")))
+        del g  # a live graph holding NCCL work blocks the communicator's teardown
+        L.tm_exchange_destroy(x)
+        a2a_ok = a2a_ok and ver.value >= 22000
 
         w = tm.CONFIGS["C1"].scaled(32, 16, 4)
         geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
@@ -135,6 +156,7 @@ def nccl_world1_worker(rank, port, out):
         out[0] = (a2a_ok, r._graph is not None, bool(np.array_equal(got7, ref7)),
                   bool(np.array_equal(got12, ref12)), r.steps_done)
         r.close()
+        halo.close_comm()
     finally:
         dist.destroy_process_group()
 
@@ -144,7 +166,7 @@ def test_nccl_capture_and_verified_replay():
     out = mgr.dict()
     mp.spawn(nccl_world1_worker, args=(free_port(), out), nprocs=1, join=True)
     a2a_ok, kept, ok7, ok12, steps = out[0]
-    assert a2a_ok, "captured all_to_all_single replay differs"
+    assert a2a_ok, "tm_halo_exchange loopback (eager or graph-captured) differs"
     assert kept, "verified capture was dropped"
     assert ok7 and ok12, "verified-capture bookkeeping advanced the wrong number of steps"
     assert steps == 12
