@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default="C2")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="strong: the config's domain split over the GPUs; weak: a slab of the config's "
+                         "per-GPU share at 8 GPUs per rank (Workload.weak)")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--zmerge", action="store_true", help="fuse z-stacked tiles into one CTA k-march")
     ap.add_argument("--unfused", action="store_true",
@@ -145,10 +148,11 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU arm: the reference path restated in C (oracle), rank 0 only
 # ---------------------------------------------------------------------------
-def cpu_reference_rate(w, budget_s: float, steps: int | None = None, boxes: int | None = None):
+def cpu_reference_rate(w, budget_s: float, steps: int | None = None, boxes: int | None = None,
+                       threads: int | None = None):
     """(rate, cores, sample description, steps run, boxes used) for the
-    reference CPU path (tag fill + four-loop tiled heat, all host threads)
-    on the first ``boxes`` boxes of the workload."""
+    reference CPU path (tag fill + four-loop tiled heat; all host threads, or
+    ``threads``) on the first ``boxes`` boxes of the workload."""
     import numpy as np
 
     from oracle import oracle as orc
@@ -156,7 +160,9 @@ def cpu_reference_rate(w, budget_s: float, steps: int | None = None, boxes: int 
     from paper_1604_03570_b200.box import decompose
     from paper_1604_03570_b200.fillplan import build_fill_plan_units
 
-    threads = orc.max_threads()
+    # every host core this process may run on (torchrun exports OMP_NUM_THREADS=1; num_threads(n)
+    # in tm_oracle.c overrides it)
+    threads = len(os.sched_getaffinity(0)) if threads is None else threads
     ba = BoxArray.chop(w.domain, w.max_grid_size)
     valids = list(ba)
     geom = Geometry(w.domain, (True, True, True), (w.dx,) * 3)
@@ -204,10 +210,12 @@ def run_reference(args, w):
     rate, cores, sample, n, nb, el = cpu_reference_rate(w, 0, steps=args.steps, boxes=boxes)
     line = {
         "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": el / n * 1e3, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": el / n * 1e3, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"{w.name}: periodic {w.n}^3, max_grid_size {w.max_grid_size}, nghost {w.nghost}, "
-                               f"ncomp {w.ncomp}, tile {w.tile_size}",
+        "config": {"workload": f"{w.name}: periodic {w.domain.extents[0]}x{w.domain.extents[1]}x"
+                               f"{w.domain.extents[2]}, max_grid_size {w.max_grid_size} "
+                               f"({len(__import__('paper_1604_03570_b200').BoxArray.chop(w.domain, w.max_grid_size))} "
+                               f"boxes), nghost {w.nghost}, ncomp {w.ncomp}, tile {w.tile_size}",
                    "sample_boxes_per_step": nb},
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -218,15 +226,49 @@ def run_reference(args, w):
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def run_ours(args, w):
+def local_slab(mf):
+    """Bounding box of this rank's boxes and whether it is exactly their union
+    (always so for the slab DistributionMapping of the BASELINE configs):
+    host transfers then move the rank's own slab only."""
+    from paper_1604_03570_b200.box import bounding_box
+
+    boxes = [mf.units[u].valid for u in mf.local_units]
+    bb = bounding_box(boxes)
+    return bb, bb.ncells == sum(b.ncells for b in boxes)
+
+
+def host_init(args, w, slab, rank):
+    """Pinned host array (ncomp, nz, ny, nx) of this rank's slab initial data.
+    Strong scaling: the config's seeded global init (SURVEY.md §8d), sliced;
+    weak scaling: seeded uniform values per rank (no rank builds the global)."""
     import numpy as np
+    import torch
+
+    import paper_1604_03570_b200 as tm
+
+    e = slab.extents
+    if args.scaling == "weak":
+        rng = np.random.default_rng(1000 + rank)
+        arr = rng.random((w.ncomp, e[2], e[1], e[0]))
+    else:
+        glob = tm.make_init(w)
+        sl = tuple(slice(slab.lo[d], slab.hi[d] + 1) for d in (2, 1, 0))
+        arr = np.ascontiguousarray(glob[(slice(None),) + sl])
+        del glob
+    return torch.from_numpy(arr).pin_memory()
+
+
+def run_ours(args, w):
     import torch
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
+    from paper_1604_03570_b200 import halo
     from paper_1604_03570_b200.runner import HeatRunner
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE is {world}")
     # one process per GPU; TM_DIST_BACKEND=gloo lets several ranks share one GPU to
     # smoke-test the multi-rank path (host-staged halos) -- never used for numbers
     backend = os.environ.get("TM_DIST_BACKEND", "nccl")
@@ -238,6 +280,8 @@ def run_ours(args, w):
         else:
             dist.init_process_group(backend)
     dev = torch.device("cuda", local)
+    if args.scaling == "weak":
+        w = w.weak(world)
 
     def barrier():
         if world > 1:
@@ -246,10 +290,12 @@ def run_ours(args, w):
 
     geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
     ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
-    glob = tm.make_init(w)
-    glob_pinned = torch.from_numpy(glob).pin_memory()
     mf = tm.MultiFab(ba, w.ncomp, w.nghost)
-    mf.from_global(glob_pinned.to(dev))
+    slab, exact = local_slab(mf)
+    if not exact:
+        raise SystemExit("bench.py: this rank's boxes do not form a slab")
+    host_in = host_init(args, w, slab, rank)
+    mf.from_global(host_in.to(dev), domain=slab)
     params = tm.HeatParams.stable(1.0, geom.dx)
     plan = tm.build_fill_plan(mf, geom)
     sched = tm.build_schedule(mf, w.tile_size)
@@ -267,8 +313,8 @@ def run_ours(args, w):
     # idle for ~0.15 s right before the timed region (clocks drop; the first ~20 steps then ran
     # ~10 % slow), so untimed steps keep it busy until the barrier; (2) a short device sleep
     # queued before ev0 lets the host enqueue the K steps' graph replays behind it, so no host
-    # issue gap is inside the timed region.  ev_mid splits the K march launches (graph replays)
-    # from the closing FillBoundary, so the kernel's launch time is measured directly.
+    # issue gap is inside the timed region.  ev_mid splits the K steps (graph replays) from the
+    # closing FillBoundary, so the step kernel's launch time is measured directly.
     stream = torch.cuda.current_stream()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev_mid = torch.cuda.Event(enable_timing=True)
@@ -285,10 +331,10 @@ def run_ours(args, w):
         barrier()
     ms = ev0.elapsed_time(ev1)
     steps_ms = ev0.elapsed_time(ev_mid)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms, steps_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max, steps_ms_max = (float(v) for v in t.tolist())
     value = total_cells * args.steps / (ms_max * 1e-3)
 
     # --- per-launch kernel times (eager, CUDA events on the launching stream) --
@@ -315,7 +361,10 @@ def run_ours(args, w):
             runner.fh.step(n, o, params)
         runner.fh.prime(runner.current, plan)
         kern_ms = timed(fused_step)
-        kern_name = "march_kernel<PACKED,SCATTER> (tm_heat_march: sweep + fused face-halo exchange)"
+        kern_name = ("march_kernel<PACKED,SCATTER,NBRH> (tm_heat_march TM_HALO_FUSED_NBR: sweep + fused "
+                     "face-halo exchange)")
+        if world > 1:
+            kern_name += " + NCCL halo exchange of remote faces"
     fill_ms = timed(lambda o, n: tm.fill_boundary(o, geom, plan))
     sweep_ms = timed(lambda o, n: tm.heat_step(n, o, geom, params, sched, zmerge=args.zmerge))
     if not runner.fused:
@@ -323,7 +372,7 @@ def run_ours(args, w):
         kern_name = "heat_step sweep (column march when eligible, else tile kernel)"
     eager_ms = kern_ms
     if runner.fused and runner.use_graph:
-        # ev0 -> ev_mid in the timed region is exactly K march launches (graph replays)
+        # ev0 -> ev_mid in the timed region is exactly K step launches (graph replays)
         kern_ms = steps_ms / args.steps
     runner.reset()  # state was advanced outside the runner's bookkeeping
     peak, peak_src = peaks()
@@ -332,10 +381,10 @@ def run_ours(args, w):
     fill_gbs = 16 * ghost_cells / (fill_ms * 1e-3) / 1e9
 
     # --- end-to-end through the public API with host buffers -------------
-    # one job = upload phi0 from pinned host memory, run the config's steps
-    # (graph replays), read back the final phi and the checksum.
+    # one job = upload this rank's slab of phi0 from pinned host memory, run the
+    # config's steps (graph replays), read back the final slab and the checksum.
     job_steps = w.steps
-    host_out = torch.empty_like(glob_pinned).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
     e2e_runs = 3
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
@@ -344,8 +393,8 @@ def run_ours(args, w):
         if it == 1:
             barrier()
             e0.record(stream)
-        g = glob_pinned.to(dev, non_blocking=True)
-        runner.a.from_global(g)
+        g = host_in.to(dev, non_blocking=True)
+        runner.a.from_global(g, domain=slab)
         runner.reset()
         out = runner.advance(job_steps)
         # the checksum (a latency-bound serial chain per box, bit-exact with the
@@ -353,7 +402,7 @@ def run_ours(args, w):
         side.wait_stream(stream)
         with torch.cuda.stream(side):
             csum = out.reduce_sum_device()
-        host_out.copy_(out.to_global())
+        host_out.copy_(out.to_global(domain=slab))
         stream.wait_stream(side)
         host_csum = float(csum.item())
     e1.record(stream)
@@ -364,68 +413,15 @@ def run_ours(args, w):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e2e_ms = float(te.item())
     e2e_value = total_cells * job_steps / (e2e_ms * 1e-3)
-    h2d = glob.nbytes
-    d2h = glob.nbytes + 8
+    h2d = host_in.numel() * 8 * world  # every rank uploads its own slab (slabs tile the domain)
+    d2h = (host_out.numel() * 8 + 8) * world
 
     # --- e2e, job stream: two jobs in flight on two CUDA streams ----------
-    # each job as above (pinned upload, steps, gather + pinned download,
-    # checksum), alternating between two runners/streams so one job's PCIe
-    # copies overlap the other's steps; host reads after the last job.
     pipe = None
     # one GPU only: concurrent graphs on two streams must not interleave one NCCL communicator
     if not args.no_pipeline and world == 1:
-        runner2 = HeatRunner(mf.clone_empty(), geom, params, sched, plan, use_graph=runner.use_graph,
-                             zmerge=args.zmerge, fused=runner.fused)
-        runners = [runner, runner2]
-        streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-        dev_in = [torch.empty_like(glob_pinned, device=dev) for _ in range(2)]
-        dev_out = [torch.zeros_like(glob_pinned, device=dev) for _ in range(2)]
-        host_outs = [torch.empty_like(glob_pinned).pin_memory() for _ in range(2)]
-        pipe_jobs = 8
-        csums = []
-
-        sides = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
-
-        def job(j):
-            r, st, sd = runners[j % 2], streams[j % 2], sides[j % 2]
-            with torch.cuda.stream(st):
-                st.wait_stream(sd)  # job j-2's checksum has read the field
-                dev_in[j % 2].copy_(glob_pinned, non_blocking=True)
-                r.a.from_global(dev_in[j % 2])
-                r.reset()
-                o = r.advance(job_steps)
-                o.to_global(out=dev_out[j % 2])
-                sd.wait_stream(st)
-                with torch.cuda.stream(sd):  # checksum beside the download
-                    csums.append(o.reduce_sum_device().clone())  # the scratch total is reused
-                host_outs[j % 2].copy_(dev_out[j % 2], non_blocking=True)
-
-        for j in range(2):  # untimed: captures runner2's graph, warms both streams
-            job(j)
-        barrier()
-        csums.clear()
-        p0 = torch.cuda.Event(enable_timing=True)
-        p1 = torch.cuda.Event(enable_timing=True)
-        p0.record(stream)
-        for st in streams + sides:
-            st.wait_stream(stream)
-        for j in range(pipe_jobs):  # job j reuses job j-2's buffers on the same stream (ordered)
-            job(j)
-        for st in streams + sides:
-            stream.wait_stream(st)
-        p1.record(stream)
-        barrier()
-        pipe_ms = p0.elapsed_time(p1) / pipe_jobs
-        tp = torch.tensor([pipe_ms], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(tp, op=dist.ReduceOp.MAX)
-        pipe_ms = float(tp.item())
-        pipe_ok = all(float(c.item()) == host_csum for c in csums) and torch.equal(host_outs[0], host_outs[1])
-        pipe = {"value": total_cells * job_steps / (pipe_ms * 1e-3), "unit": UNIT, "jobs": pipe_jobs,
-                "in_flight": 2, "ms_per_job": pipe_ms, "checksums_match_serial": bool(pipe_ok),
-                "how": "same job as e2e; jobs alternate over two runners / CUDA streams so uploads and "
-                       "downloads overlap the other job's steps"}
-        runner2.close()
+        pipe = pipelined_e2e(runner, HeatRunner, mf, geom, params, sched, plan, args, host_in, slab, job_steps,
+                             host_csum, total_cells, barrier, dev, stream)
         runner.reset()
 
     line = None
@@ -433,29 +429,41 @@ def run_ours(args, w):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             rate, cores, sample, _, _, _ = cpu_reference_rate(w, args.cpu_seconds)
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+            rate1, _, sample1, _, _, _ = cpu_reference_rate(w, args.cpu_seconds / 2, threads=1)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+                   "one_core": {"value": rate1, "cores": 1, "sample": sample1}}
         traffic = profile_traffic(w.name, runner.fused)
         launches_per_step = runner.launches_per_step
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic" + (" (seeded uniform per rank)" if args.scaling == "weak" else
+                                   " (seeded init of BASELINE.json's config)"),
             "config": {
-                "workload": f"{w.name}: periodic {w.n}^3, max_grid_size {w.max_grid_size} ({len(ba)} boxes), "
-                            f"nghost {w.nghost}, ncomp {w.ncomp}, tile {w.tile_size}, seeded gauss+noise init",
+                "workload": f"{w.name}: periodic {w.domain.extents[0]}x{w.domain.extents[1]}x{w.domain.extents[2]}, "
+                            f"max_grid_size {w.max_grid_size} ({len(ba)} boxes), nghost {w.nghost}, "
+                            f"ncomp {w.ncomp}, tile {w.tile_size}",
                 "step": "FillBoundary + heat sweep over all boxes",
-                "l2": f"inputs larger than L2: {2 * total_cells * 8 / 1e6:.0f} MB streamed per step vs 126 MB L2",
-                "parallelism": f"dm{world} (contiguous box slabs)", "cuda_graph": runner.use_graph,
-                "zmerge": args.zmerge,
-                "step_impl": ("fused: one persistent column-march launch per step; the epilogue writes face halos "
-                              "of the next step (FillBoundary fused), edges/corners refreshed by one FillBoundary "
-                              "per advance()" if runner.fused else
+                "l2": f"inputs larger than L2: {2 * local_cells * 8 / 1e6:.0f} MB streamed per step per GPU "
+                      f"vs 126 MB L2",
+                "parallelism": f"dm{world} (contiguous box slabs, one process per GPU, NCCL halo exchange)",
+                "cuda_graph": runner.use_graph, "zmerge": args.zmerge,
+                "step_impl": ("fused: one persistent column-march launch per step; y/z halos read from the face "
+                              "neighbours' valid cells, x halos from packed buffers the previous step's epilogue "
+                              "wrote (FillBoundary fused); edges/corners refreshed by one FillBoundary per "
+                              "advance()" if runner.fused else
                               "FillBoundary kernel + tiled heat sweep (2 launches per step)"),
             },
             "roofline": {
                 "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "kernel": kern_name,
+                "traffic": traffic,
+                "traffic_note": "ncu dram__bytes_read+write of one cold launch (profiles/ncu_summary.json, static); "
+                                "write-back of the last ~40 MB lands after the kernel ends",
+                "kernel": kern_name,
                 "bytes_per_launch": BYTES_PER_CELL * local_cells, "avg_launch_ms": kern_ms,
+                "avg_launch_ms_how": "timed region ev0->ev_mid (K graph-replayed step launches) / K"
+                if runner.fused and runner.use_graph else "eager launches between CUDA events",
                 "eager_launch_ms": eager_ms,
                 "peak_source": peak_src,
             },
@@ -464,7 +472,8 @@ def run_ours(args, w):
                                    "note": "reference step structure, for comparison"},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d / job_steps,
                     "d2h_bytes_per_step": d2h / job_steps,
-                    "job": f"upload phi0 (pinned) + {job_steps} steps + download phi + checksum",
+                    "job": f"each rank uploads its slab of phi0 (pinned) + {job_steps} steps + downloads its slab "
+                           f"+ checksum",
                     "ms_per_job": e2e_ms, "checksum": host_csum, "pipelined": pipe},
             "gpu_launches": launches_per_step * args.steps + (1 if runner.fused else 0),
             "clocks": clocks.summary(),
@@ -473,17 +482,93 @@ def run_ours(args, w):
             line["cpu_baseline"] = cpu
         print(json.dumps(line), flush=True)
     runner.close()  # before the process group goes: a live graph may hold NCCL work
+    halo.close_comm()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def pipelined_e2e(runner, HeatRunner, mf, geom, params, sched, plan, args, host_in, slab, job_steps, host_csum,
+                  total_cells, barrier, dev, stream):
+    """The e2e job stream with two jobs in flight: each job as in ``e2e``
+    (pinned upload, steps, gather + pinned download, checksum), alternating
+    between two runners / CUDA streams so one job's PCIe copies overlap the
+    other's steps; host reads after the last job."""
+    import torch
+
+    runner2 = HeatRunner(mf.clone_empty(), geom, params, sched, plan, use_graph=runner.use_graph,
+                         zmerge=args.zmerge, fused=runner.fused)
+    runners = [runner, runner2]
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    dev_in = [torch.empty_like(host_in, device=dev) for _ in range(2)]
+    dev_out = [torch.zeros_like(host_in, device=dev) for _ in range(2)]
+    host_outs = [torch.empty_like(host_in).pin_memory() for _ in range(2)]
+    pipe_jobs = 8
+    csums = []
+    sides = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+
+    def job(j):
+        r, st, sd = runners[j % 2], streams[j % 2], sides[j % 2]
+        with torch.cuda.stream(st):
+            st.wait_stream(sd)  # job j-2's checksum has read the field
+            dev_in[j % 2].copy_(host_in, non_blocking=True)
+            r.a.from_global(dev_in[j % 2], domain=slab)
+            r.reset()
+            o = r.advance(job_steps)
+            o.to_global(domain=slab, out=dev_out[j % 2])
+            sd.wait_stream(st)
+            with torch.cuda.stream(sd):  # checksum beside the download
+                csums.append(o.reduce_sum_device().clone())  # the scratch total is reused
+            host_outs[j % 2].copy_(dev_out[j % 2], non_blocking=True)
+
+    for j in range(2):  # untimed: captures runner2's graph, warms both streams
+        job(j)
+    barrier()
+    csums.clear()
+    p0 = torch.cuda.Event(enable_timing=True)
+    p1 = torch.cuda.Event(enable_timing=True)
+    p0.record(stream)
+    for st in streams + sides:
+        st.wait_stream(stream)
+    for j in range(pipe_jobs):  # job j reuses job j-2's buffers on the same stream (ordered)
+        job(j)
+    for st in streams + sides:
+        stream.wait_stream(st)
+    p1.record(stream)
+    barrier()
+    pipe_ms = p0.elapsed_time(p1) / pipe_jobs
+    pipe_ok = all(float(c.item()) == host_csum for c in csums) and torch.equal(host_outs[0], host_outs[1])
+    runner2.close()
+    return {"value": total_cells * job_steps / (pipe_ms * 1e-3), "unit": UNIT, "jobs": pipe_jobs,
+            "in_flight": 2, "ms_per_job": pipe_ms, "checksums_match_serial": bool(pipe_ok),
+            "how": "same job as e2e; jobs alternate over two runners / CUDA streams so uploads and "
+                   "downloads overlap the other job's steps"}
+
+
+def spawn_ranks(args) -> int:
+    """``--gpus N`` outside torchrun: launch N single-GPU ranks of this script
+    (torch.distributed.run, rendezvous on 127.0.0.1) and pass their output
+    through; rank 0 prints the JSON line."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
     args = parse()
     from paper_1604_03570_b200.configs import CONFIGS
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     w = CONFIGS[args.config]
     if args.impl == "reference":
+        if args.scaling == "weak":
+            w = w.weak(args.gpus)
         run_reference(args, w)
     else:
         run_ours(args, w)

@@ -42,10 +42,11 @@ class Workload:
     kernel: str  # "heat" or "gsrb"
     init: str
     seed: int = 0
+    nz: int | None = None  # z extent when the domain is not a cube (weak-scaled slabs)
 
     @property
     def domain(self) -> Box:
-        return Box((0, 0, 0), (self.n - 1,) * 3)
+        return Box((0, 0, 0), (self.n - 1, self.n - 1, (self.nz or self.n) - 1))
 
     @property
     def dx(self) -> float:
@@ -53,7 +54,17 @@ class Workload:
 
     @property
     def cells(self) -> int:
-        return self.n ** 3
+        return self.n * self.n * (self.nz or self.n)
+
+    def weak(self, ranks: int) -> "Workload":
+        """Weak-scaled slab domain: n x n x (L * max_grid_size * ranks), L box
+        layers per rank -- the config's per-GPU share at 8 GPUs (C5: 4 layers
+        of 32^3 boxes, so 8 ranks hold the full C5; C2 / C3: one layer).
+        Uniform random init (the values do not change any code path)."""
+        layers = max(1, self.n // self.max_grid_size // 8)
+        return Workload(f"{self.name}-weak{ranks}", self.n, self.max_grid_size, self.nghost, self.ncomp,
+                        self.tile_size, self.steps, self.kernel, "uniform", self.seed,
+                        nz=layers * self.max_grid_size * ranks)
 
     def scaled(self, n: int, max_grid_size: int | None = None, steps: int | None = None) -> "Workload":
         """Same workload shape at a smaller domain (parity tests)."""
@@ -111,6 +122,8 @@ def make_init(w: Workload) -> np.ndarray:
     """Global initial data ``(ncomp, nz, ny, nx)`` for a workload (phi, or
     rhs for the Poisson config)."""
     n = w.n
+    if w.nz not in (None, n) and w.init != "uniform":
+        raise ValueError(f"init {w.init!r} is defined on cubic domains only")
     rng = np.random.default_rng(w.seed)
     shape = (n, n, n)
     if w.init == "gauss_noise":
@@ -119,9 +132,10 @@ def make_init(w: Workload) -> np.ndarray:
         phi = (1.0 + gaussian(n)) + 1e-3 * noise
         return phi.reshape((1,) + shape)
     if w.init == "uniform":
+        shape = ((w.nz or n), n, n)
         out = np.empty((w.ncomp,) + shape)
         for c in range(w.ncomp):
-            out[c] = rng.random(n ** 3).reshape(shape)
+            out[c] = rng.random(int(np.prod(shape))).reshape(shape)
         return out
     if w.init == "uniform_bump":
         out = np.empty((w.ncomp,) + shape)

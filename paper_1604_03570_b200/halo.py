@@ -118,8 +118,12 @@ class HaloExchange:
         for ids in recvs.values():
             for n in ids:
                 self.remote_dst.setdefault(tags[n][0], []).append(tags[n][1])
-        # local units whose valid cells some other rank needs
-        self.send_units = sorted({tags[n][2] for ids in sends.values() for n in ids})
+        # local units whose valid cells some other rank needs, and those cells (source boxes)
+        self.send_src: dict = {}
+        for ids in sends.values():
+            for n in ids:
+                self.send_src.setdefault(tags[n][2], []).append(tags[n][3])
+        self.send_units = sorted(self.send_src)
         pack_tags, self.send_spans, nsend = build(sends, True)
         unpack_tags, self.recv_spans, nrecv = build(recvs, False)
         self.pack = _native.CopyPlan(pack_tags, nc)

@@ -248,6 +248,40 @@ def xh_own_ghost_plan(mf: MultiFab, sides, nyv: int, nzv: int):
     return _native.CopyPlan(tags, mf.ncomp), (1, 2 * nyv, 2 * nyv * nzv)
 
 
+def split_columns_by_sends(mf: MultiFab, cols: np.ndarray, send_src: dict):
+    """Split march columns (full z extent) into (boundary, interior) column
+    pieces along z: a piece is boundary when its planes hold cells that some
+    send tag reads (``send_src``: unit -> source boxes, global indices).  A
+    piece is a column with its own z range (tm_block z0 / nz), so both sets
+    are ordinary march plans; every plane lands in exactly one of them."""
+    L = mf.layout
+    bnd, inner = [], []
+    for c in cols:
+        s, y0, z0, ny, nz = int(c["slot"]), int(c["y0"]), int(c["z0"]), int(c["ny"]), int(c["nz"])
+        u = mf.local_units[s]
+        v = mf.units[u].valid
+        ylo = v.lo[1] + y0 - L.nghost
+        zlo = v.lo[2] + z0 - L.nghost
+        hit = np.zeros(nz, dtype=bool)
+        for b in send_src.get(u, ()):
+            if b.hi[1] < ylo or b.lo[1] > ylo + ny - 1:
+                continue  # the column's rows miss this source box (columns span the full x extent)
+            k0, k1 = max(b.lo[2] - zlo, 0), min(b.hi[2] - zlo, nz - 1)
+            if k0 <= k1:
+                hit[k0:k1 + 1] = True
+        k = 0
+        while k < nz:
+            e = k
+            while e < nz and hit[e] == hit[k]:
+                e += 1
+            piece = c.copy()
+            piece["z0"], piece["nz"] = z0 + k, e - k
+            (bnd if hit[k] else inner).append(piece)
+            k = e
+    mk = lambda rows: np.array(rows, dtype=_native.BLOCK_DTYPE) if rows else np.zeros(0, dtype=_native.BLOCK_DTYPE)  # noqa: E731
+    return mk(bnd), mk(inner)
+
+
 class FusedHalo:
     """Packed x halos + neighbour table shared by an old/new MultiFab pair."""
 
@@ -282,9 +316,11 @@ class FusedHalo:
         cols = self.plan.columns
         nbr_ok = len(set(cols["ny"].tolist())) == 1 and int(cols["nx"].max()) % 16 == 0
         self.mode = _native.HALO_FUSED_NBR if nbr_ok else _native.HALO_FUSED_SCATTER
-        # Multi-rank: the columns of boxes with a face on another rank ("boundary" boxes) march
-        # first; their faces travel on a side stream while the remaining columns march, so the
-        # NCCL exchange overlaps the interior sweep.  Each column is still
+        # Multi-rank: the column planes holding cells another rank needs (the source cells of the
+        # halo exchange: remote faces, edges, corners) march first as one launch; they travel on a
+        # side stream while every other plane marches as a second launch, so the NCCL exchange
+        # overlaps the interior sweep even when every box touches another
+        # rank (C2 strong-scaled: only its boundary planes / rows wait).  Each cell is still
         # computed exactly once, by the same kernel, so results do not change.
         self.plan_b = self.plan_i = None
         self.comm = None
@@ -298,13 +334,10 @@ class FusedHalo:
 
             fp = fill_plan = fill_plan if fill_plan is not None else _bfp(a, geom)
             halo = _device_fill(a, fp)[1]
-            src_units = set(halo.send_units) if halo is not None else set()
-            bslots = np.array(sorted({a.slot_of[u] for u in src_units} |
-                                     set(np.nonzero((table == REMOTE).any(axis=1))[0].tolist())), dtype=np.int64)
-            isb = np.isin(cols["slot"], bslots)
-            if isb.any() and (~isb).any():
-                self.plan_b = _native.MarchPlan(cols[isb], self.plan.nctas)
-                self.plan_i = _native.MarchPlan(cols[~isb], self.plan.nctas)
+            bcols, icols = split_columns_by_sends(a, cols, halo.send_src if halo is not None else {})
+            if len(bcols) and len(icols):
+                self.plan_b = _native.MarchPlan(bcols, self.plan.nctas)
+                self.plan_i = _native.MarchPlan(icols, self.plan.nctas)
                 self.comm = torch.cuda.Stream(a.device)
         # faces whose neighbour is on another rank: filled by the halo exchange after each
         # step; x faces then copied from the ghost column into the packed x halo

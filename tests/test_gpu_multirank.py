@@ -26,7 +26,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, out, fused, slabs=False):
+def worker(rank, world, port, out, fused, shape=(48, 16)):
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
@@ -37,9 +37,10 @@ def worker(rank, world, port, out, fused, slabs=False):
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        # 27 boxes split mid-layer, or 216 boxes = three z-layers per rank (the middle one
-        # has no remote face: its columns march while the boundary faces are exchanged)
-        w = tm.CONFIGS["C5"].scaled(48, 8 if slabs else 16, 4)  # 2 comps, 2 ghosts
+        # (48, 16): 27 boxes split mid-layer; (48, 8): 216 boxes = three z-layers per rank (the
+        # middle one has no remote face); (64, 32): one z-layer of 4 boxes per rank, every box
+        # touching the other rank (only their non-boundary planes overlap the exchange)
+        w = tm.CONFIGS["C5"].scaled(shape[0], shape[1], 4)  # 2 comps, 2 ghosts
         geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
         ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
         glob = tm.make_init(w)
@@ -50,7 +51,9 @@ def worker(rank, world, port, out, fused, slabs=False):
         assert r.fused == fused and not r.use_graph
         if fused:  # the 27 boxes split mid-layer: remote neighbours in x, y and z
             assert r.fh.remote
-            assert (r.fh.comm is not None) == slabs  # boundary / interior launches + side stream
+            # boundary planes / interior planes as two launches + side stream, also when every box
+            # touches the other rank (27 boxes split mid-layer)
+            assert r.fh.comm is not None
         fin = r.advance(w.steps)
         got = fin.to_global().cpu().numpy()  # only this rank's boxes are non-zero
         c = p.coefficients()
@@ -70,19 +73,19 @@ def worker(rank, world, port, out, fused, slabs=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("fused,slabs", [(False, False), (True, False), (True, True)])
-def test_two_ranks_one_gpu_match_oracle(fused, slabs):
+@pytest.mark.parametrize("fused,shape", [(False, (48, 16)), (True, (48, 16)), (True, (48, 8)), (True, (64, 32))])
+def test_two_ranks_one_gpu_match_oracle(fused, shape):
     """fused=False: the overlapped unfused step; fused=True: the fused march
     with the remote faces exchanged after each step (slabs: on a side stream,
     overlapping the interior columns' launch)."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(worker, args=(2, free_port(), out, fused, slabs), nprocs=2, join=True)
+    mp.spawn(worker, args=(2, free_port(), out, fused, shape), nprocs=2, join=True)
     for r in range(2):
         ok, sums_ok, max_ok, min_ok, n = out[r]
         assert ok, f"rank {r}: boxes differ from the oracle"
         assert sums_ok and max_ok and min_ok, f"rank {r}: reductions differ"
-    assert out[0][4] + out[1][4] == (216 if slabs else 27)
+    assert out[0][4] + out[1][4] == (shape[0] // shape[1]) ** 3
 
 
 def nccl_world1_worker(rank, port, out):
