@@ -103,6 +103,14 @@ int tm_copy_plan_destroy(tm_copy_plan *plan);
 int64_t tm_copy_plan_elements(const tm_copy_plan *plan); /* cells x ncomp */
 int tm_copy_run(const tm_copy_plan *plan, double *dst, const tm_side *dst_side, const double *src,
                 const tm_side *src_side, void *stream);
+/* x-face ghosts (first ghost layer, valid y/z range) of every slot from a
+ * packed x-halo buffer xh[(slot*ncomp+c)][z][side][y] as written by
+ * tm_heat_march's TM_HALO_GHOSTS_XH / fused modes (side 0 -> x = lo-1, side 1
+ * -> x = hi+1; uniform valid x extent nx; nghost == 1).  Each ghost is written as a whole
+ * 64-B chunk of its row (the ghost plus row padding nothing reads).  Together
+ * with tm_copy_run over the remaining tags it is the whole FillBoundary
+ * (level.py:297-323) of a field whose packed x halos are current. */
+int tm_xh_to_ghosts(const tm_layout *layout, double *base, const double *xh, int32_t nx, void *stream);
 
 /* ---- stencil sweeps -------------------------------------------------------- */
 int tm_sweep_plan_create(const tm_block *blocks, int64_t nblocks, tm_sweep_plan **out);
@@ -140,6 +148,12 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  *   TM_HALO_GHOSTS        x/y/z halos from the ghost cells of uold (FillBoundary
  *                         must have run); writes only valid cells of unew.
  *                         xh_old, xh_new, d_nbr must be NULL, reverse 0.
+ *   TM_HALO_GHOSTS_XH     as GHOSTS (halos read from uold's ghost cells), and the
+ *                         epilogue also writes the packed x halos of unew's
+ *                         boxes into xh_new (d_nbr as below): unew's storage
+ *                         is written on valid cells only -- the reference's
+ *                         heat_step contract -- and the next step may take its
+ *                         x halos from xh_new.
  *   TM_HALO_PACKED        x halos from the packed buffer xh_old
  *                         xh[(slot*ncomp+c)][z][side][y] (valid y,z extents;
  *                         side 0 = i = lo-1, side 1 = i = hi+1), y/z from the
@@ -167,7 +181,7 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  * may overlap the previous kernel on the stream; it waits (griddepcontrol.wait)
  * for that kernel to complete before touching uold/unew, so stream order is
  * preserved. */
-enum { TM_HALO_GHOSTS = 0, TM_HALO_PACKED = 1, TM_HALO_FUSED_SCATTER = 2, TM_HALO_FUSED_NBR = 3 };
+enum { TM_HALO_GHOSTS = 0, TM_HALO_PACKED = 1, TM_HALO_FUSED_SCATTER = 2, TM_HALO_FUSED_NBR = 3, TM_HALO_GHOSTS_XH = 4 };
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);

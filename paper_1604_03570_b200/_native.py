@@ -23,7 +23,7 @@ TM_ERR_CUDA = 2
 ABI_VERSION = 3
 
 # halo_mode of tm_heat_march (include/tilemesh_b200.h)
-HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR = 0, 1, 2, 3
+HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR, HALO_GHOSTS_XH = 0, 1, 2, 3, 4
 
 
 class tm_layout(ctypes.Structure):
@@ -45,7 +45,7 @@ assert COPY_TAG_DTYPE.itemsize == 32 and BLOCK_DTYPE.itemsize == 32
 
 EXPORTS = [
     "tm_last_error", "tm_abi_version", "tm_device_check",
-    "tm_copy_plan_create", "tm_copy_plan_destroy", "tm_copy_plan_elements", "tm_copy_run",
+    "tm_copy_plan_create", "tm_copy_plan_destroy", "tm_copy_plan_elements", "tm_copy_run", "tm_xh_to_ghosts",
     "tm_sweep_plan_create", "tm_sweep_plan_destroy", "tm_heat_sweep", "tm_gsrb_color",
     "tm_residual_maxnorm", "tm_reduce_sum", "tm_reduce_minmax",
     "tm_march_plan_create", "tm_march_plan_destroy", "tm_march_plan_reset_halos", "tm_heat_march", "tm_gsrb_march", "tm_wide4_march",
@@ -86,6 +86,7 @@ def load():
     L.tm_copy_plan_elements.argtypes = [vp]
     L.tm_copy_plan_elements.restype = i64
     L.tm_copy_run.argtypes = [vp, vp, P(tm_side), vp, P(tm_side), vp]
+    L.tm_xh_to_ghosts.argtypes = [P(tm_layout), vp, vp, i32, vp]
     L.tm_sweep_plan_create.argtypes = [vp, i64, P(vp)]
     L.tm_sweep_plan_destroy.argtypes = [vp]
     L.tm_heat_sweep.argtypes = [vp, P(tm_layout), vp, vp, i32, i32, f64, f64, f64, f64, vp]

@@ -154,6 +154,37 @@ struct tm_copy_plan {
     int grid = 0;
 };
 
+// x-face ghost columns (one layer) from a packed x-halo buffer: the two x
+// faces of every FillBoundary are the costly ones in this layout (each 8-B
+// ghost and each 8-B source value sits in its own DRAM chunk); when the step
+// that produced the field also wrote xh[(slot*ncomp+c)][z][side][y] (its
+// neighbours' boundary columns, dense), the ghosts are written from it:
+// dense reads, and one full 64-B chunk per ghost row (the ghost plus row
+// padding nothing reads), so no write is a read-modify-write.  Thread =
+// (row, side) with y fastest: the xh reads coalesce.
+__global__ void __launch_bounds__(256) xh_ghosts_kernel(double *__restrict__ base, const double *__restrict__ xh,
+                                                       int64_t pitch, int64_t plane, int64_t comp_stride,
+                                                       int32_t xlo, int32_t xhi, int32_t nyv, int32_t nzv,
+                                                       int32_t y0, int32_t z0, int64_t rows) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * rows; t += stride) {
+        // t = ((w * nzv + z) * 2 + side) * nyv + y: the xh element order
+        const int64_t y = t % nyv;
+        const int64_t r = t / nyv;
+        const int side = (int)(r & 1);
+        const int64_t wz = r >> 1;
+        const int64_t z = wz % nzv, w = wz / nzv;
+        const double v = xh[t];
+        double *row = base + w * comp_stride + (z + z0) * plane + (y + y0) * pitch;
+        double2 *chunk = reinterpret_cast<double2 *>(row + (side ? xhi : xlo - 8));
+        const double2 pad = make_double2(0.0, 0.0);
+        chunk[0] = side ? make_double2(v, 0.0) : pad;
+        chunk[1] = pad;
+        chunk[2] = pad;
+        chunk[3] = side ? pad : make_double2(0.0, v);
+    }
+}
+
 extern "C" {
 
 int tm_copy_plan_create(const tm_copy_tag *tags, int64_t ntags, int32_t ncomp, tm_copy_plan **out) {
@@ -225,6 +256,31 @@ int tm_copy_run(const tm_copy_plan *plan, double *dst, const tm_side *dst_side, 
                                                                                    plan->ntasks);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tm_copy_run launch");
+    return TM_OK;
+}
+
+int tm_xh_to_ghosts(const tm_layout *layout, double *base, const double *xh, int32_t nx, void *stream) {
+    using namespace tmk;
+    int rc = check_layout(layout, "tm_xh_to_ghosts");
+    if (rc) return rc;
+    const tm_layout &L = *layout;
+    if (!base || !xh || nx < 1) return fail(TM_ERR_INVALID, "tm_xh_to_ghosts: bad arguments");
+    if (L.nghost != 1)  // the 64-B chunks overwrite the row padding, where deeper ghost layers live
+        return fail(TM_ERR_INVALID, "tm_xh_to_ghosts: needs nghost == 1");
+    const int32_t xlo = L.xoff, xhi = L.xoff + nx;
+    if (xhi % 2 || xhi + 8 > L.pitch || xlo < 8)
+        return fail(TM_ERR_INVALID, "tm_xh_to_ghosts: the 64-B ghost chunks must lie inside the row padding");
+    const int32_t nyv = L.ny - 2 * L.nghost, nzv = L.nz - 2 * L.nghost;
+    const int64_t rows = L.nslots * L.ncomp * (int64_t)nyv * nzv;
+    if (rows == 0) return TM_OK;
+    const Strides st = strides_of(L);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t blocks = std::min<int64_t>((2 * rows + 255) / 256, (int64_t)sms * 8);
+    xh_ghosts_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(base, xh, st.row, st.plane, st.comp, xlo, xhi,
+                                                                      nyv, nzv, L.nghost, L.nghost, rows);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_fail(e, "xh_ghosts_kernel launch");
     return TM_OK;
 }
 

@@ -72,6 +72,14 @@ __device__ __forceinline__ void issue(const CUtensorMap *map, const CUtensorMap 
     }
 }
 
+// One plane as a consumer warp needs it: its RPW rows of CPL cells per lane
+// and their in-plane flux sums.
+template <int CPL, int RPW, bool HS>
+struct PlaneRegs {
+    double u[RPW][CPL];                        // the warp's cells
+    double hs[HS ? RPW : 1][HS ? CPL : 1];     // their in-plane flux sums (x and y parts)
+};
+
 // NBRH (fused mode, uniform columns): the z halo planes and the y halo rows at
 // box faces are read straight from the face neighbour's valid cells in uold
 // (the same values a FillBoundary would have copied into our ghosts), so the
@@ -125,6 +133,10 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                                                                  const __grid_constant__ CUtensorMap rmap,
                                                                  MarchArgs a) {
     static_assert(!NBRH || (PACKED && SCATTER), "neighbour-sourced halos belong to the fused mode");
+    // SCATTER: the epilogue writes the packed x halos of the new field (xh_new); with x halos
+    // from the packed buffer and y/z halos from ghost cells (TM_HALO_FUSED_SCATTER) it also
+    // writes the y/z face ghosts of unew.  TM_HALO_GHOSTS_XH (!PACKED) writes xh_new only.
+    constexpr bool kYZ = SCATTER && PACKED && !NBRH;
     using namespace tmk;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double *stages = reinterpret_cast<double *>(smem_raw);
@@ -259,12 +271,12 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         int kz_lo = -1, kz_hi = -1;
         int64_t zoff_lo = 0, zoff_hi = 0;
         if (SCATTER) {
-            if (!NBRH && warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
+            if (kYZ && warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
                 ylo_i = 0;
                 ylo = orow[0] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
             }
             const int rl = c.ny - 1;  // last row of the column
-            if (!NBRH && yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
+            if (kYZ && yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
                 yhi_i = rl % RPW;
                 yhi = obase + (int64_t)rl * st.row + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
             }
@@ -277,11 +289,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                       warp * RPW;
                 x_right = true;
             }
-            if (!NBRH && nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
+            if (kYZ && nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
                 kz_lo = -zl0;
                 zoff_lo = (int64_t)(nb[4] - c.slot) * st.slot + (int64_t)nzb * st.plane;
             }
-            if (!NBRH && nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
+            if (kYZ && nb[5] >= 0 && zl0 <= nzb - 1 && nzb - 1 < zl0 + nk) {
                 kz_hi = nzb - 1 - zl0;
                 zoff_hi = (int64_t)(nb[5] - c.slot) * st.slot - (int64_t)nzb * st.plane;
             }
@@ -293,81 +305,120 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         uint64_t xh_addr = reinterpret_cast<uint64_t>(xhp);
 
         // priming: planes k0-1 and k0 -> carried z flux and centre values
-        double ua[RPW][CPL], ub[RPW][CPL], fzm[RPW][CPL];
-        wait_plane(g);
-        wait_plane(g + 1);
-        {
-            const uint32_t s0 = saddr(g), s1 = saddr(g + 1);
-#pragma unroll
-            for (int i = 0; i < RPW; ++i)
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    // forward: s0 = plane k0-1, s1 = k0, carry fz- of k0; REV: s0 = plane k1,
-                    // s1 = k1-1, carry fz+ of k1-1 (u[k+1] - u[k] either way)
-                    const double lo = lds_f64(s0 + roff[i] + 8u * j), hi = lds_f64(s1 + roff[i] + 8u * j);
-                    ua[i][j] = hi;
-                    fzm[i][j] = REV ? rn_mul(rn_sub(lo, hi), c2) : rn_mul(rn_sub(hi, lo), c2);
-                }
-        }
-        release(g);
-        // one plane: centre values in cur, next-plane values land in nxt
-        auto plane = [&](int kk, double (&cur)[RPW][CPL], double (&nxt)[RPW][CPL]) {
-            const uint32_t gc = g + 1 + (uint32_t)kk;
-            const uint32_t sc = saddr(gc), sn = saddr(gc + 1);
-            wait_plane(gc + 1);
-            // y fluxes between consecutive rows are shared by the two rows (same bits)
-            double fy[RPW + 1][CPL];
-            {
-                double ym[CPL], yp[CPL];
-#pragma unroll
-                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
-                    if constexpr (CPL >= 2) {
-                        lds_f64x2(sc + roff[0] - ystep + 8u * j, ym[j], ym[j + 1]);
-                        lds_f64x2(sc + ypo + 8u * j, yp[j], yp[j + 1]);
-                    } else {
-                        ym[j] = lds_f64(sc + roff[0] - ystep + 8u * j);
-                        yp[j] = lds_f64(sc + ypo + 8u * j);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    fy[0][j] = rn_mul(rn_sub(cur[0][j], ym[j]), c1);
-#pragma unroll
-                    for (int i = 1; i < RPW; ++i) fy[i][j] = rn_mul(rn_sub(cur[i][j], cur[i - 1][j]), c1);
-                    fy[RPW][j] = rn_mul(rn_sub(yp[j], cur[RPW - 1][j]), c1);
-                }
-            }
-            double out[RPW][CPL];
+        // Early release (kEarly, instances whose registers allow it): when a plane lands, the
+        // warp reads everything it needs from it -- its rows, the rows just above and below,
+        // the x neighbours of its row ends -- computes the plane's in-plane flux sums
+        // hs = (fx+ - fx-)*dxi0 + (fy+ - fy-)*dxi1 (the first half of the reference's sum,
+        // same operation order), and hands the stage back at once: every stage but the one
+        // being read stays in flight.  Every loaded value is consumed by that arithmetic
+        // before the release, so the stage is never overwritten under an outstanding read.
+        // Otherwise the centre plane's stage is held through the arithmetic (half the ring in
+        // flight).
+        constexpr bool kEarly = CPL * RPW <= 4;
+        PlaneRegs<CPL, RPW, kEarly> pa, pb;
+        double fzm[RPW][CPL];
+        auto load_u = [&](uint32_t sb, PlaneRegs<CPL, RPW, kEarly> &P) {
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
                     if constexpr (CPL >= 2)
-                        lds_f64x2(sn + roff[i] + 8u * j, nxt[i][j], nxt[i][j + 1]);
+                        lds_f64x2(sb + roff[i] + 8u * j, P.u[i][j], P.u[i][j + 1]);
                     else
-                        nxt[i][j] = lds_f64(sn + roff[i] + 8u * j);
+                        P.u[i][j] = lds_f64(sb + roff[i] + 8u * j);
                 }
-                const double xl = lds_f64(sc + xlo[i]);
-                const double xr = lds_f64(sc + xro[i]);
-                double fx[CPL + 1];
-                fx[0] = rn_mul(rn_sub(cur[i][0], xl), c0);
+            }
+        };
+        // in-plane flux sums of plane sb for the warp's cells (y fluxes between consecutive
+        // rows are shared by the two rows; x fluxes between a lane's cells shared likewise)
+        auto inplane = [&](uint32_t sb, const double (&u)[RPW][CPL], double (&hs)[RPW][CPL]) {
+            double ym[CPL], yp[CPL];
 #pragma unroll
-                for (int j = 1; j < CPL; ++j) fx[j] = rn_mul(rn_sub(cur[i][j], cur[i][j - 1]), c0);
-                fx[CPL] = rn_mul(rn_sub(xr, cur[i][CPL - 1]), c0);
+            for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                if constexpr (CPL >= 2) {
+                    lds_f64x2(sb + roff[0] - ystep + 8u * j, ym[j], ym[j + 1]);
+                    lds_f64x2(sb + ypo + 8u * j, yp[j], yp[j + 1]);
+                } else {
+                    ym[j] = lds_f64(sb + roff[0] - ystep + 8u * j);
+                    yp[j] = lds_f64(sb + ypo + 8u * j);
+                }
+            }
+            double fy[RPW + 1][CPL];
+#pragma unroll
+            for (int j = 0; j < CPL; ++j) {
+                fy[0][j] = rn_mul(rn_sub(u[0][j], ym[j]), c1);
+#pragma unroll
+                for (int i = 1; i < RPW; ++i) fy[i][j] = rn_mul(rn_sub(u[i][j], u[i - 1][j]), c1);
+                fy[RPW][j] = rn_mul(rn_sub(yp[j], u[RPW - 1][j]), c1);
+            }
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                const double xl = lds_f64(sb + xlo[i]);
+                const double xr = lds_f64(sb + xro[i]);
+                double fx[CPL + 1];
+                fx[0] = rn_mul(rn_sub(u[i][0], xl), c0);
+#pragma unroll
+                for (int j = 1; j < CPL; ++j) fx[j] = rn_mul(rn_sub(u[i][j], u[i][j - 1]), c0);
+                fx[CPL] = rn_mul(rn_sub(xr, u[i][CPL - 1]), c0);
+#pragma unroll
+                for (int j = 0; j < CPL; ++j)
+                    hs[i][j] = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
+            }
+        };
+        auto fetch = [&](uint32_t q, PlaneRegs<CPL, RPW, kEarly> &P) {
+            wait_plane(q);
+            const uint32_t sb = saddr(q);
+            load_u(sb, P);
+            if constexpr (kEarly) {
+                double(&hs)[RPW][CPL] = P.hs;
+                inplane(sb, P.u, hs);
+                release(q);
+            }
+        };
+        {
+            // priming: plane k0-1 (forward; k1 reversed) for the carried z flux, then plane k0
+            wait_plane(g);
+            const uint32_t s0 = saddr(g);
+            double lo[RPW][CPL];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j) lo[i][j] = lds_f64(s0 + roff[i] + 8u * j);
+            fetch(g + 1, pa);
+#pragma unroll
+            for (int i = 0; i < RPW; ++i)
+#pragma unroll
+                for (int j = 0; j < CPL; ++j)  // u[k+1] - u[k] in either direction
+                    fzm[i][j] = REV ? rn_mul(rn_sub(lo[i][j], pa.u[i][j]), c2) : rn_mul(rn_sub(pa.u[i][j], lo[i][j]), c2);
+            release(g);  // after lo[][] has been consumed
+        }
+        // one plane: centre values in cur, the next plane lands in nxt
+        auto plane = [&](int kk, PlaneRegs<CPL, RPW, kEarly> &cur, PlaneRegs<CPL, RPW, kEarly> &nxt) {
+            const uint32_t gc = g + 1 + (uint32_t)kk;
+            double hsl[RPW][CPL];  // non-early instances: the centre plane's flux sums, computed here
+            if constexpr (!kEarly) inplane(saddr(gc), cur.u, hsl);
+            fetch(gc + 1, nxt);
+            double out[RPW][CPL];
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
-                    const double u0 = cur[i][j];
+                    const double u0 = cur.u[i][j];
                     // fresh z flux toward the next plane; fzm[][] carries the other one
-                    const double fnew = REV ? rn_mul(rn_sub(u0, nxt[i][j]), c2) : rn_mul(rn_sub(nxt[i][j], u0), c2);
+                    const double fnew =
+                        REV ? rn_mul(rn_sub(u0, nxt.u[i][j]), c2) : rn_mul(rn_sub(nxt.u[i][j], u0), c2);
                     const double fzp = REV ? fzm[i][j] : fnew, fzn = REV ? fnew : fzm[i][j];
-                    double sum = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
-                    sum = rn_add(sum, rn_mul(rn_sub(fzp, fzn), c2));
+                    double hs;
+                    if constexpr (kEarly)
+                        hs = cur.hs[i][j];
+                    else
+                        hs = hsl[i][j];
+                    const double sum = rn_add(hs, rn_mul(rn_sub(fzp, fzn), c2));
                     out[i][j] = rn_add(u0, rn_mul(c3, sum));
                     fzm[i][j] = fnew;
                 }
             }
-            // all shared reads of the centre plane are done: hand its stage back early
-            release(gc);
+            if constexpr (!kEarly) release(gc);  // all shared reads of the centre plane are done
             auto st_cells = [&](double *d, int i) {
 #pragma unroll
                 for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
@@ -381,14 +432,14 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
             for (int i = 0; i < RPW; ++i) {
                 if (!on[i]) continue;
                 st_cells(orow[i] + koff, i);
-                if (SCATTER && !NBRH) {
+                if (kYZ) {
                     if (i == ylo_i) st_cells(ylo + koff, i);
                     if (i == yhi_i) st_cells(yhi + koff, i);
                 }
             }
             if (SCATTER) {
                 const int kz = REV ? nk - 1 - kk : kk;  // plane index from k0
-                if (!NBRH && (kz == kz_lo || kz == kz_hi)) {  // warp-uniform, two planes per column
+                if (kYZ && (kz == kz_lo || kz == kz_hi)) {  // warp-uniform, two planes per column
                     const int64_t zd = kz == kz_lo ? zoff_lo : zoff_hi;
 #pragma unroll
                     for (int i = 0; i < RPW; ++i)
@@ -411,11 +462,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         };
         int kk = 0;
         for (; kk + 1 < nk; kk += 2) {  // ping-pong: no register rotation
-            plane(kk, ua, ub);
-            plane(kk + 1, ub, ua);
+            plane(kk, pa, pb);
+            plane(kk + 1, pb, pa);
         }
-        if (kk < nk) plane(kk, ua, ub);
-        release(g + nk + 1);
+        if (kk < nk) plane(kk, pa, pb);
+        if constexpr (!kEarly) release(g + nk + 1);
         g += nk + 2;
     }
 }
@@ -887,8 +938,10 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march: bad ncomp");
     if (strides_of(L).comp >= ((int64_t)1 << 32))
         return fail(TM_ERR_INVALID, "tm_heat_march: one component of a slot must hold < 2^32 doubles");
-    const bool packed = halo_mode != TM_HALO_GHOSTS;
-    const bool scatter = halo_mode == TM_HALO_FUSED_SCATTER || halo_mode == TM_HALO_FUSED_NBR;
+    const bool packed = halo_mode == TM_HALO_PACKED || halo_mode == TM_HALO_FUSED_SCATTER ||
+                        halo_mode == TM_HALO_FUSED_NBR;
+    const bool scatter = halo_mode == TM_HALO_FUSED_SCATTER || halo_mode == TM_HALO_FUSED_NBR ||
+                         halo_mode == TM_HALO_GHOSTS_XH;
     switch (halo_mode) {
         case TM_HALO_GHOSTS:
             if (xh_old || xh_new || d_nbr || reverse)
@@ -897,6 +950,10 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
         case TM_HALO_PACKED:
             if (!xh_old || xh_new || d_nbr || reverse)
                 return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_PACKED needs xh_old only");
+            break;
+        case TM_HALO_GHOSTS_XH:
+            if (xh_old || !xh_new || !d_nbr)
+                return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_GHOSTS_XH needs xh_new and d_nbr, no xh_old");
             break;
         case TM_HALO_FUSED_SCATTER:
         case TM_HALO_FUSED_NBR:
@@ -910,7 +967,8 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (!p->even) return fail(TM_ERR_INVALID, "tm_heat_march: columns must start on even x and have even width");
     const int cpl = p->max_nx <= 32 ? 1 : (p->max_nx <= 64 ? 2 : 4);
     if (cpl == 4 && (p->max_nx % 4)) return fail(TM_ERR_INVALID, "tm_heat_march: widths > 64 must be multiples of 4");
-    if (packed && p->max_ny % 2) return fail(TM_ERR_INVALID, "tm_heat_march: packed x halo needs even column height");
+    if ((packed || scatter) && p->max_ny % 2)
+        return fail(TM_ERR_INVALID, "tm_heat_march: packed x halos need even column heights");
     // neighbour-sourced y/z halos: the column rows and the two halo rows are separate TMA boxes,
     // each landing on a stage row that must be 128-B aligned (TMA destination)
     if (halo_mode == TM_HALO_FUSED_NBR && !(p->uniform_ny && p->max_nx % 16 == 0))
@@ -957,6 +1015,8 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
         p->last_halo_mode = halo_mode;
         p->last_xh_new = xh_new;
     }
+    if (halo_mode == TM_HALO_GHOSTS_XH)
+        return launch_march<false, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
     switch (halo_mode) {
         case TM_HALO_GHOSTS:
             return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);

@@ -183,7 +183,7 @@ class HaloExchange:
             self.recvbuf[:self.nrecv].copy_(self._hrecv)
         else:
             torch.cuda.current_stream(self.device).wait_stream(self._side)
-        self.unpack.run(mf.ptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)
+        self.unpack.run(mf.gptr, mf.layout.side(), self.recvbuf.data_ptr(), (0, 0, 0), stream)
 
     def _nccl_exchange(self):
         """The library-side plan of this exchange's messages (``tm_exchange``:

@@ -135,20 +135,73 @@ def march_plan(mf: MultiFab, packed: bool = False, max_rows: int | None = None,
 
 
 def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None = None,
-               nctas: int | None = None) -> None:
-    """One sweep (all components) with x halos from the ghost columns of
-    ``mf_old``; FillBoundary must have run.  Bit-identical to heat_step."""
+               nctas: int | None = None, geom: Geometry | None = None) -> None:
+    """One sweep (all components); FillBoundary must have run, as for the
+    reference's heat_step.  Bit-identical to heat_step.
+
+    With ``geom`` and a one-rank layout of uniform boxes whose faces all have a
+    neighbour box, the sweep also writes ``mf_new``'s packed x halos
+    (``MultiFab.xh_buffer``: no storage cell beyond the valid ones), and when
+    ``mf_old``'s packed x halos and ghosts are both current (the previous
+    heat_step wrote the halos, a FillBoundary ran since, nothing else wrote the
+    field) it reads y/z halos from the face neighbours' valid cells and x halos
+    from the packed buffer -- the fused bench kernel -- instead of the ghost
+    columns: the same values, fewer DRAM sectors.  ``fill_boundary`` likewise
+    writes the x-face ghosts of a field with current packed halos from them."""
     if mf_old.nghost < 1:
         raise ValueError("heat kernel requires nghost >= 1")
     if not mf_new.same_layout(mf_old):
         raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
     if not march_eligible(mf_old):
-        raise ValueError("column march needs boxes of even x extent <= 128")
-    plan = march_plan(mf_old, False, max_rows, nctas)
+        raise ValueError("column march needs boxes of even x extent <= 128 (a multiple of 4 beyond 64)")
     c = params.coefficients()
-    _native.check(_native.load().tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr,
-                                               mf_old.ncomp, c[0], c[1], c[2], c[3], _native.HALO_GHOSTS,
-                                               None, None, None, 0, mf_old.stream()), "tm_heat_march")
+    L = _native.load()
+    route = xh_route(mf_old, geom) if geom is not None and max_rows is None and nctas is None else None
+    if route is None:
+        plan = march_plan(mf_old, False, max_rows, nctas)
+        _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.wptr,
+                                      mf_old.ncomp, c[0], c[1], c[2], c[3], _native.HALO_GHOSTS,
+                                      None, None, None, 0, mf_old.stream()), "tm_heat_march")
+        return
+    nbr, nbr_plan = route
+    xh_new = mf_new.xh_buffer()
+    if nbr_plan is not None and mf_old.xh_current() and mf_old.ghosts_current():
+        plan, mode, xh_old = nbr_plan, _native.HALO_FUSED_NBR, mf_old._xh.data_ptr()
+        _native.check(L.tm_march_plan_reset_halos(plan.handle), "tm_march_plan_reset_halos")
+    else:
+        plan, mode, xh_old = march_plan(mf_old, False), _native.HALO_GHOSTS_XH, None
+    _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.wptr, mf_old.ncomp,
+                                  c[0], c[1], c[2], c[3], mode, xh_old, xh_new.data_ptr(), nbr.data_ptr(), 0,
+                                  mf_old.stream()), "tm_heat_march")
+    mf_new._xh_key = mf_new.valid_key()
+
+
+def default_fused_rows(mf: MultiFab):
+    """Column height of the fused kernels: boxes wider than 64 run 4 cells per
+    lane in 32-row columns, one 17-warp CTA per SM (C3, 128-wide boxes: 1.71
+    -> 1.60 ms/step against 8-row columns at 2 CTAs/SM; tools/march_perf.py
+    --config C3); otherwise ``max_rows_for``'s choice (None)."""
+    return 32 if max(mf.units[u].valid.extents[0] for u in mf.local_units) > 64 else None
+
+
+def xh_route(mf: MultiFab, geom: Geometry):
+    """(face-neighbour table on the device, march plan of the neighbour-halo
+    mode or None) when heat_step may keep packed x halos for this layout (one
+    rank, fusable), else None.  Cached per MultiFab and geometry."""
+    key = ("xh_route", geom)
+    if key not in mf._plans:
+        route = None
+        if mf.dm.nranks == 1 and fusable(mf, geom):
+            import torch
+
+            table = face_neighbors(mf, geom)
+            nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=mf.device)
+            plan = march_plan(mf, True, default_fused_rows(mf))
+            cols = plan.columns
+            ok = len(set(cols["ny"].tolist())) == 1 and int(cols["nx"].max()) % 16 == 0
+            route = (nbr, plan if ok else None)
+        mf._plans[key] = route
+    return mf._plans[key]
 
 
 # --------------------------------------------------------------------------
@@ -304,10 +357,8 @@ class FusedHalo:
                    id(b): torch.zeros(shape, dtype=torch.float64, device=a.device)}
         table = face_neighbors(a, geom, multi)
         self.nbr = torch.as_tensor(table.reshape(-1), dtype=torch.int32, device=a.device)
-        if max_rows is None and max(a.units[u].valid.extents[0] for u in a.local_units) > 64:
-            # 4 cells per lane: 32-row columns, one 17-warp CTA per SM (C3, 128-wide boxes: 1.71 ->
-            # 1.60 ms/step against 8-row columns at 2 CTAs/SM; tools/march_perf.py --config C3)
-            max_rows = 32
+        if max_rows is None:
+            max_rows = default_fused_rows(a)
         self.plan = march_plan(a, True, max_rows, nctas)
         # Halo mode (include/tilemesh_b200.h): with columns of one height and 128-B aligned
         # rows the y/z halos are read from the neighbours' valid cells and the epilogue writes
@@ -381,7 +432,7 @@ class FusedHalo:
 
         def march(plan):
             _native.check(_native.load().tm_heat_march(
-                plan.handle, old.layout.to_c(), old.ptr, new.ptr, old.ncomp, c[0], c[1], c[2], c[3], self.mode,
+                plan.handle, old.layout.to_c(), old.ptr, new.wptr, old.ncomp, c[0], c[1], c[2], c[3], self.mode,
                 self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
                 old.stream()), "tm_heat_march(fused)")
 
@@ -454,7 +505,7 @@ class FusedGSRB:
     def colour(self, color: int) -> None:
         phi, rhs = self.phi, self.rhs
         _native.check(_native.load().tm_gsrb_march(
-            self.plan.handle, phi.layout.to_c(), phi.ptr, rhs.layout.to_c(), rhs.ptr, color, self.h2,
+            self.plan.handle, phi.layout.to_c(), phi.wptr, rhs.layout.to_c(), rhs.ptr, color, self.h2,
             self.xh.data_ptr(), self.nbr.data_ptr(), phi.stream()), "tm_gsrb_march")
 
     def sweep(self) -> None:
@@ -563,6 +614,6 @@ class SplitGSRB:
 
         phi = self.phi
         _native.check(_native.load().tm_gsrb_merge(
-            phi.layout.to_c(), phi.ptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
+            phi.layout.to_c(), phi.wptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
             self.c[1].data_ptr(), phi.stream()), "tm_gsrb_merge")
         fill_boundary(phi, self.geom, plan)

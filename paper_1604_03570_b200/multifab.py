@@ -210,6 +210,16 @@ class MultiFab:
         self._plans: dict = {}
         self._unit_sweep = None
         self._scratch = {}
+        # State keys of the reference-loop fast path (heat_step / fill_boundary):
+        # ``valid_key`` changes whenever valid cells may have changed -- any torch in-place
+        # write to ``data`` or a view of it (torch's version counter) or a library kernel
+        # writing through ``wptr``; ``_xh_key`` is the valid_key for which the packed x
+        # halos ``_xh`` hold the neighbours' boundary columns; ``_fill_key`` the valid_key
+        # at the end of the last complete FillBoundary (ghosts consistent with valid data).
+        self._writes = 0
+        self._xh = None
+        self._xh_key = None
+        self._fill_key = None
 
     # ------------------------------------------------------------------ misc
     def clone_empty(self) -> "MultiFab":
@@ -228,7 +238,41 @@ class MultiFab:
 
     @property
     def ptr(self) -> int:
+        """Device address of the storage, for kernels that only READ it."""
         return self.data.data_ptr()
+
+    @property
+    def wptr(self) -> int:
+        """Device address for a kernel that writes valid cells (invalidates the
+        packed x halos and the filled-ghost state)."""
+        self._writes += 1
+        return self.data.data_ptr()
+
+    @property
+    def gptr(self) -> int:
+        """Device address for a kernel that writes ghost cells only (a fill or
+        halo unpack; valid cells, and so the packed x halos, are unchanged)."""
+        self._fill_key = None
+        return self.data.data_ptr()
+
+    def valid_key(self) -> tuple:
+        return (self.data._version, self._writes)
+
+    def xh_buffer(self):
+        """Packed x halos of this field: (slot*ncomp+c, nz, 2, ny) over valid y/z."""
+        import torch
+
+        if self._xh is None:
+            L = self.layout
+            self._xh = torch.empty((L.nslots * self.ncomp, L.nz - 2 * L.nghost, 2, L.ny - 2 * L.nghost),
+                                   dtype=torch.float64, device=self.device)
+        return self._xh
+
+    def xh_current(self) -> bool:
+        return self._xh is not None and self._xh_key == self.valid_key()
+
+    def ghosts_current(self) -> bool:
+        return self._fill_key is not None and self._fill_key == self.valid_key()
 
     def stream(self) -> int:
         return _native.stream_handle(self.device)
@@ -288,7 +332,7 @@ class MultiFab:
         if tuple(g.shape) != (self.ncomp, n[2], n[1], n[0]):
             raise ValueError(f"global array shape {tuple(g.shape)} != {(self.ncomp, n[2], n[1], n[0])}")
         plan, gs = self._global_copy_plan(domain, "scatter")
-        plan.run(self.ptr, self.layout.side(), g.data_ptr(), gs, self.stream())
+        plan.run(self.wptr, self.layout.side(), g.data_ptr(), gs, self.stream())
         self._keepalive = g
 
     def to_global(self, domain: Box | None = None, out=None):
@@ -344,7 +388,7 @@ class MultiFab:
             sh = (shadow, _native.CopyPlan(tags, self.ncomp))
             self._plans["grid_shadow"] = sh
         shadow, plan = sh
-        plan.run(shadow.ptr, shadow.layout.side(), self.ptr, self.layout.side(), self.stream())
+        plan.run(shadow.wptr, shadow.layout.side(), self.ptr, self.layout.side(), self.stream())
         return shadow
 
     # -------------------------------------------------------------- reductions
@@ -554,16 +598,57 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
         if plan is None:
             plan = build_fill_plan(mf, geom)
             mf._plans[("fill", geom)] = plan
-    copy, halo = _device_fill(mf, plan)
     stream = mf.stream()
-    if halo is not None:
-        halo.start(mf, stream)
-    copy.run(mf.ptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
-    if halo is not None:
-        halo.finish(mf, stream)
+    fast = _xh_fill(mf, plan) if mf.xh_current() else None
+    if fast is not None:
+        # the x faces come from the packed x halos the last heat step wrote (dense reads),
+        # every other tag from the copy kernel
+        copy, nx = fast
+        copy.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
+        _native.check(_native.load().tm_xh_to_ghosts(mf.layout.to_c(), mf.gptr, mf._xh.data_ptr(), nx, stream),
+                      "tm_xh_to_ghosts")
+    else:
+        copy, halo = _device_fill(mf, plan)
+        if halo is not None:
+            halo.start(mf, stream)
+        copy.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
+        if halo is not None:
+            halo.finish(mf, stream)
+    mf._fill_key = mf.valid_key()
 
 
 FillBoundary = fill_boundary
+
+
+def _xh_fill(mf: MultiFab, plan: FillPlan):
+    """(copy plan of every tag except the x-face ghost columns, box width) for a
+    one-rank, one-ghost MultiFab of uniform boxes, or None.  The x faces are
+    then written by ``tm_xh_to_ghosts`` from the packed x halos."""
+    key = ("xh_fill",) + _plan_key(mf)
+    if key in plan._device:
+        return plan._device[key]
+    out = None
+    widths = {mf.units[u].valid.extents for u in mf.local_units}
+    if mf.nghost == 1 and mf.dm.nranks == 1 and len(widths) == 1:
+        nx, ny, nz = next(iter(widths))
+        L = mf.layout
+        keep = []
+        covered = 0
+        for t in plan.tags:
+            v = mf.units[t.dst_unit].valid
+            d = t.dst_box
+            xface = (d.extents[0] == 1 and d.lo[0] in (v.lo[0] - 1, v.hi[0] + 1)
+                     and v.lo[1] <= d.lo[1] and d.hi[1] <= v.hi[1] and v.lo[2] <= d.lo[2] and d.hi[2] <= v.hi[2])
+            if xface:
+                covered += d.ncells
+            else:
+                keep.append(t)
+        # every x-face ghost must come from a tag (fully periodic or fully covered), or the
+        # kernel would write cells the reference leaves alone
+        if covered == 2 * ny * nz * len(mf.local_units) and (L.xoff + nx) % 2 == 0 and L.xoff + nx + 8 <= L.pitch:
+            out = (_native.CopyPlan(local_copy_tags(mf, keep), mf.ncomp), nx)
+    plan._device[key] = out
+    return out
 
 
 # --------------------------------------------------------------------------

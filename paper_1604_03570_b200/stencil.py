@@ -108,7 +108,7 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
     if _use_march(mf_old, zmerge):
         from .march import heat_march
 
-        heat_march(mf_new, mf_old, params)
+        heat_march(mf_new, mf_old, params, geom=geom)
         return
     sched = _schedule_for(mf_old, schedule)
     plan = schedule_sweep_plan(mf_old, sched, zmerge)
@@ -116,7 +116,7 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
         return
     dxi0, dxi1, dxi2, dtD = params.coefficients()
     L = _native.load()
-    _native.check(L.tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr, 0, mf_old.ncomp,
+    _native.check(L.tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.wptr, 0, mf_old.ncomp,
                                   dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
 
 
@@ -126,7 +126,7 @@ def heat_sweep_plan(mf_new: MultiFab, mf_old: MultiFab, params: HeatParams, plan
     if plan.nblocks == 0:
         return
     dxi0, dxi1, dxi2, dtD = params.coefficients()
-    _native.check(_native.load().tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.ptr, 0,
+    _native.check(_native.load().tm_heat_sweep(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.wptr, 0,
                                                mf_old.ncomp, dxi0, dxi1, dxi2, dtD, mf_old.stream()),
                   "tm_heat_sweep")
 
@@ -143,12 +143,12 @@ def overlapped_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: 
     copy, halo = _device_fill(mf_old, plan)
     stream = mf_old.stream()
     if halo is None:
-        copy.run(mf_old.ptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
+        copy.run(mf_old.gptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
         heat_step(mf_new, mf_old, geom, params, schedule, zmerge=zmerge)
         return
     inner, outer = overlap_sweep_plans(mf_old, schedule, halo.remote_dst, zmerge)
     halo.start(mf_old, stream)
-    copy.run(mf_old.ptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
+    copy.run(mf_old.gptr, mf_old.layout.side(), mf_old.ptr, mf_old.layout.side(), stream)
     heat_sweep_plan(mf_new, mf_old, params, inner)
     halo.finish(mf_old, stream)
     heat_sweep_plan(mf_new, mf_old, params, outer)
@@ -174,7 +174,7 @@ def gsrb_color(phi: MultiFab, rhs: MultiFab, geom: Geometry, color: int,
     plan = schedule_sweep_plan(phi, _schedule_for(phi, schedule))
     if plan.nblocks == 0:
         return
-    _native.check(_native.load().tm_gsrb_color(plan.handle, phi.layout.to_c(), phi.ptr, rhs.layout.to_c(),
+    _native.check(_native.load().tm_gsrb_color(plan.handle, phi.layout.to_c(), phi.wptr, rhs.layout.to_c(),
                                                rhs.ptr, color, h2, phi.stream()), "tm_gsrb_color")
 
 
