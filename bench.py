@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU-baseline sample length")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-pipeline", action="store_true", help="skip the two-jobs-in-flight e2e variant")
+    ap.add_argument("--configs", default="C3,C4,C5",
+                    help="other BASELINE configs measured after the headline at N=1 ('' to skip)")
     ap.add_argument("--hot-steps", type=int, default=2000,
                     help="untimed steps run right before the timed region (keeps clocks up)")
     return ap.parse_args()
@@ -433,6 +435,7 @@ def run_ours(args, w):
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                    "one_core": {"value": rate1, "cores": 1, "sample": sample1}}
         traffic = profile_traffic(w.name, runner.fused)
+        others = config_records(args, peak) if world == 1 and args.configs else None
         launches_per_step = runner.launches_per_step
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -480,6 +483,8 @@ def run_ours(args, w):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if others is not None:
+            line["other_configs"] = others
         print(json.dumps(line), flush=True)
     runner.close()  # before the process group goes: a live graph may hold NCCL work
     halo.close_comm()
@@ -543,6 +548,73 @@ def pipelined_e2e(runner, HeatRunner, mf, geom, params, sched, plan, args, host_
             "in_flight": 2, "ms_per_job": pipe_ms, "checksums_match_serial": bool(pipe_ok),
             "how": "same job as e2e; jobs alternate over two runners / CUDA streams so uploads and "
                    "downloads overlap the other job's steps"}
+
+
+def config_records(args, peak):
+    """BASELINE.json's other configs on this GPU (N=1), so their rates are in the
+    driver's record and not only in the builder's logs: C3 and C5 heat (fused,
+    chained steps, graph-replayed; device-side uniform init -- the values change no
+    code path) and C4 (GSRB solve, colour-split).  Each: cell-updates/s over K steps
+    timed with CUDA events (inputs larger than L2), and the fraction of the HBM peak
+    on the algorithmic bytes (16 B per heat update, 24 B per GSRB update).  A config
+    that fails reports its error instead of a number."""
+    import torch
+
+    import paper_1604_03570_b200 as tm
+    from paper_1604_03570_b200.runner import HeatRunner
+
+    out = {}
+
+    def timed(fn, reps):
+        torch.cuda.synchronize()
+        torch.cuda._sleep(400_000)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn(reps)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    for name in args.configs.split(","):
+        name = name.strip()
+        if not name:
+            continue
+        w = tm.CONFIGS[name]
+        try:
+            geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+            ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+            cells = w.cells * w.ncomp
+            if w.kernel == "heat":
+                mf = tm.MultiFab(ba, w.ncomp, w.nghost, zero=False)
+                mf.data.uniform_()
+                r = HeatRunner(mf, geom, tm.HeatParams.stable(1.0, geom.dx), w.tile_size)
+                k = max(4, min(w.steps, 20))
+                r.advance(k)  # warm-up: plans, graph capture
+                ms = timed(lambda n: r.advance(n, finalize=False), k)
+                rec = {"value": cells / (ms * 1e-3), "ms_per_step": ms, "steps": k,
+                       "roofline_frac": 16 * cells / (ms * 1e-3) / 1e9 / peak, "bytes_per_update": 16,
+                       "step_impl": "fused chained" if r.chain else ("fused" if r.fused else "unfused")}
+                r.close()
+                del r, mf
+            else:
+                phi = tm.MultiFab(ba, 1, 1)
+                rhs = tm.MultiFab(ba, 1, 0)
+                rhs.from_global(tm.make_init(w))
+                tm.gsrb_solve(phi, rhs, geom, 2)  # warm-up
+                ms = timed(lambda n: tm.gsrb_solve(phi, rhs, geom, n), w.steps)
+                rec = {"value": cells / (ms * 1e-3), "ms_per_sweep": ms, "sweeps": w.steps,
+                       "roofline_frac": 24 * cells / (ms * 1e-3) / 1e9 / peak, "bytes_per_update": 24,
+                       "residual": tm.residual_maxnorm(phi, rhs, geom),
+                       "note": "per sweep incl. the solve's split/merge and closing FillBoundary"}
+                del phi, rhs
+            rec["workload"] = (f"{name}: periodic {w.n}^3, max_grid_size {w.max_grid_size} ({len(ba)} boxes), "
+                               f"nghost {w.nghost}, ncomp {w.ncomp}")
+            rec["unit"] = UNIT
+            out[name] = rec
+        except Exception as e:  # noqa: BLE001 -- reported, the headline line still prints
+            out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
+    return out
 
 
 def spawn_ranks(args) -> int:
