@@ -103,13 +103,12 @@ int tm_copy_plan_destroy(tm_copy_plan *plan);
 int64_t tm_copy_plan_elements(const tm_copy_plan *plan); /* cells x ncomp */
 int tm_copy_run(const tm_copy_plan *plan, double *dst, const tm_side *dst_side, const double *src,
                 const tm_side *src_side, void *stream);
-/* x-face ghosts (first ghost layer, valid y/z range) of every slot from a
- * packed x-halo buffer xh[(slot*ncomp+c)][z][side][y] as written by
- * tm_heat_march's TM_HALO_GHOSTS_XH / fused modes (side 0 -> x = lo-1, side 1
- * -> x = hi+1; uniform valid x extent nx; nghost == 1).  Each ghost is written as a whole
- * 64-B chunk of its row (the ghost plus row padding nothing reads).  Together
- * with tm_copy_run over the remaining tags it is the whole FillBoundary
- * (level.py:297-323) of a field whose packed x halos are current. */
+/* x-face ghosts (one ghost layer, valid y/z range) of every slot from a
+ * packed x-halo buffer xh[(slot*ncomp+c)][z][side][y] as tm_heat_march writes
+ * it for a field (side 0 -> x = lo-1, side 1 -> x = hi+1; uniform valid x
+ * extent nx; nghost == 1).  Each ghost is written as a whole 64-B chunk of its
+ * row (the ghost plus row padding nothing reads).  The x-face part of
+ * fill_boundary (level.py:297-323) for a field whose packed halos are known. */
 int tm_xh_to_ghosts(const tm_layout *layout, double *base, const double *xh, int32_t nx, void *stream);
 
 /* ---- stencil sweeps -------------------------------------------------------- */
@@ -168,6 +167,13 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  *                         x halos from xh_old; the epilogue writes ONLY xh_new.
  *                         The y/z face ghosts of unew are NOT written.  Needs
  *                         columns of one height and width % 16 == 0.
+ *   TM_HALO_FUSED_NBR_GHOSTS  as FUSED_NBR (forward, nghost 1), and the y/z
+ *                         halo rows and planes it loads -- exactly the y/z face
+ *                         ghosts of uold a FillBoundary writes -- are also
+ *                         stored into uold's ghosts (faces with a local
+ *                         neighbour): the y/z face part of a preceding
+ *                         fill_boundary, deferred into the sweep.  The only
+ *                         mode that writes through `uold`.
  * The fused modes are the FillBoundary of the next step fused into this one
  * (face halos only: the 7-point stencil never reads edge/corner ghosts).  A
  * SCATTER step must not follow an NBR step on the same packed halos (the y/z
@@ -181,7 +187,14 @@ int tm_march_plan_destroy(tm_march_plan *plan);
  * may overlap the previous kernel on the stream; it waits (griddepcontrol.wait)
  * for that kernel to complete before touching uold/unew, so stream order is
  * preserved. */
-enum { TM_HALO_GHOSTS = 0, TM_HALO_PACKED = 1, TM_HALO_FUSED_SCATTER = 2, TM_HALO_FUSED_NBR = 3, TM_HALO_GHOSTS_XH = 4 };
+enum {
+    TM_HALO_GHOSTS = 0,
+    TM_HALO_PACKED = 1,
+    TM_HALO_FUSED_SCATTER = 2,
+    TM_HALO_FUSED_NBR = 3,
+    TM_HALO_GHOSTS_XH = 4,
+    TM_HALO_FUSED_NBR_GHOSTS = 5
+};
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);

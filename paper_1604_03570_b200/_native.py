@@ -23,7 +23,7 @@ TM_ERR_CUDA = 2
 ABI_VERSION = 3
 
 # halo_mode of tm_heat_march (include/tilemesh_b200.h)
-HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR, HALO_GHOSTS_XH = 0, 1, 2, 3, 4
+HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR, HALO_GHOSTS_XH, HALO_FUSED_NBR_GHOSTS = 0, 1, 2, 3, 4, 5
 
 
 class tm_layout(ctypes.Structure):

@@ -114,6 +114,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// 32-B global store (one full DRAM sector; sm_100 256-bit STG)
+__device__ __forceinline__ void st_global_f64x4(double *p, double a, double b, double c, double d) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 // predicated 16-B global store (no branch around it)
 __device__ __forceinline__ void st_global_f64x2_if(uint64_t addr, double a, double b, bool pred) {
     asm volatile(

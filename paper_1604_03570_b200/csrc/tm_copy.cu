@@ -154,21 +154,18 @@ struct tm_copy_plan {
     int grid = 0;
 };
 
-// x-face ghost columns (one layer) from a packed x-halo buffer: the two x
-// faces of every FillBoundary are the costly ones in this layout (each 8-B
-// ghost and each 8-B source value sits in its own DRAM chunk); when the step
-// that produced the field also wrote xh[(slot*ncomp+c)][z][side][y] (its
-// neighbours' boundary columns, dense), the ghosts are written from it:
-// dense reads, and one full 64-B chunk per ghost row (the ghost plus row
-// padding nothing reads), so no write is a read-modify-write.  Thread =
-// (row, side) with y fastest: the xh reads coalesce.
+// x-face ghost columns (one layer) from a packed x-halo buffer (tm_xh_to_ghosts).  Four
+// consecutive threads write the four 16-B pieces of one row's 64-B chunk in the same
+// instruction (a warp: 8 whole chunks), so every chunk reaches L2 as one full write.
 __global__ void __launch_bounds__(256) xh_ghosts_kernel(double *__restrict__ base, const double *__restrict__ xh,
                                                        int64_t pitch, int64_t plane, int64_t comp_stride,
                                                        int32_t xlo, int32_t xhi, int32_t nyv, int32_t nzv,
                                                        int32_t y0, int32_t z0, int64_t rows) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < 2 * rows; t += stride) {
+    for (int64_t t4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t4 < 8 * rows; t4 += stride) {
         // t = ((w * nzv + z) * 2 + side) * nyv + y: the xh element order
+        const int64_t t = t4 >> 2;
+        const int piece = (int)(t4 & 3);
         const int64_t y = t % nyv;
         const int64_t r = t / nyv;
         const int side = (int)(r & 1);
@@ -177,11 +174,9 @@ __global__ void __launch_bounds__(256) xh_ghosts_kernel(double *__restrict__ bas
         const double v = xh[t];
         double *row = base + w * comp_stride + (z + z0) * plane + (y + y0) * pitch;
         double2 *chunk = reinterpret_cast<double2 *>(row + (side ? xhi : xlo - 8));
-        const double2 pad = make_double2(0.0, 0.0);
-        chunk[0] = side ? make_double2(v, 0.0) : pad;
-        chunk[1] = pad;
-        chunk[2] = pad;
-        chunk[3] = side ? pad : make_double2(0.0, v);
+        // the ghost is the chunk's first double on the right (x = hi+1), its last on the left
+        const bool holds = side ? piece == 0 : piece == 3;
+        chunk[piece] = holds ? (side ? make_double2(v, 0.0) : make_double2(0.0, v)) : make_double2(0.0, 0.0);
     }
 }
 
@@ -276,7 +271,7 @@ int tm_xh_to_ghosts(const tm_layout *layout, double *base, const double *xh, int
     const Strides st = strides_of(L);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    const int64_t blocks = std::min<int64_t>((2 * rows + 255) / 256, (int64_t)sms * 8);
+    const int64_t blocks = std::min<int64_t>((8 * rows + 255) / 256, (int64_t)sms * 8);
     xh_ghosts_kernel<<<(unsigned)blocks, 256, 0, as_stream(stream)>>>(base, xh, st.row, st.plane, st.comp, xlo, xhi,
                                                                       nyv, nzv, L.nghost, L.nghost, rows);
     cudaError_t e = cudaGetLastError();

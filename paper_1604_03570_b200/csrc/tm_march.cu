@@ -47,6 +47,7 @@ struct MarchArgs {
     int32_t xh_off;                     // offset of the x-halo slice inside a stage (PACKED)
     int32_t nyv, nzv;                   // packed x-halo extents (valid y, z of a slot)
     double *xh_new;                     // SCATTER: packed x halo of the new field
+    double *gw;                         // GW: uold's storage, whose face ghosts the step fills
     const int32_t *nbr;                 // SCATTER: 6 neighbour slots per slot (-x,+x,-y,+y,-z,+z)
 };
 
@@ -127,12 +128,17 @@ __device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensor
 // bytes); empty[s] completes when all NWARP consumer warps released it.  No
 // CTA-wide barrier in the steady state: fast warps run ahead up to the ring
 // depth while the producer refills each stage as soon as it is free.
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH>
+// GW (TM_HALO_FUSED_NBR_GHOSTS): the y/z halo rows and planes the neighbour-halo step loads
+// are exactly the y/z face ghosts a FillBoundary of uold writes, so the step also stores them
+// into uold's ghosts -- the deferred y/z part of the preceding fill_boundary
+// (multifab.fill_boundary), at no extra read.  Other CTAs read only uold's valid cells.
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW = false>
 __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const __grid_constant__ CUtensorMap xmap,
                                                                  const __grid_constant__ CUtensorMap rmap,
                                                                  MarchArgs a) {
     static_assert(!NBRH || (PACKED && SCATTER), "neighbour-sourced halos belong to the fused mode");
+    static_assert(!GW || (NBRH && !REV), "face-ghost writes ride on the forward neighbour-halo step");
     // SCATTER: the epilogue writes the packed x halos of the new field (xh_new); with x halos
     // from the packed buffer and y/z halos from ghost cells (TM_HALO_FUSED_SCATTER) it also
     // writes the y/z face ghosts of unew.  TM_HALO_GHOSTS_XH (!PACKED) writes xh_new only.
@@ -303,6 +309,20 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         // RPW == 2: rows come in pairs (even column heights), so on[0] == on[1]
         const bool xh_on = xhp != nullptr && on[0];
         uint64_t xh_addr = reinterpret_cast<uint64_t>(xhp);
+        // GW targets (uold's y/z face ghosts, faces with a local neighbour only): the y ghost row
+        // above / below the column by the warp holding its first / last row, the z ghost planes
+        // from the priming / last halo plane.  (x faces: the packed halos ARE those ghosts; the
+        // host keeps them as a snapshot instead of scattering 8-B values over every row.)
+        double *gbase = nullptr;
+        bool gy_lo = false, gy_hi = false, gz_lo = false, gz_hi = false;
+        if (GW) {
+            // koff addresses the column's first row: this warp's rows start warp*RPW rows below
+            gbase = a.gw + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)warp * RPW * st.row;
+            gy_lo = lane_on && warp == 0 && yl0 == 0 && nb[2] >= 0;
+            gy_hi = lane_on && warp * RPW + RPW - 1 == c.ny - 1 && yl0 + c.ny == nyb && nb[3] >= 0;
+            gz_lo = zl0 == 0 && nb[4] >= 0;
+            gz_hi = zl0 + nk == nzb && nb[5] >= 0;
+        }
 
         // priming: planes k0-1 and k0 -> carried z flux and centre values
         // Early release (kEarly, instances whose registers allow it): when a plane lands, the
@@ -331,7 +351,8 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         };
         // in-plane flux sums of plane sb for the warp's cells (y fluxes between consecutive
         // rows are shared by the two rows; x fluxes between a lane's cells shared likewise)
-        auto inplane = [&](uint32_t sb, const double (&u)[RPW][CPL], double (&hs)[RPW][CPL]) {
+        auto inplane = [&](uint32_t sb, const double (&u)[RPW][CPL], double (&hs)[RPW][CPL], uint32_t goff,
+                           bool centre) {
             double ym[CPL], yp[CPL];
 #pragma unroll
             for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
@@ -341,6 +362,28 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                 } else {
                     ym[j] = lds_f64(sb + roff[0] - ystep + 8u * j);
                     yp[j] = lds_f64(sb + ypo + 8u * j);
+                }
+            }
+            if (GW && centre) {
+                if (gy_lo) {
+#pragma unroll
+                    for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                        double *d = gbase + goff - st.row + j;
+                        if constexpr (CPL >= 2)
+                            *reinterpret_cast<double2 *>(d) = make_double2(ym[j], ym[j + 1]);
+                        else
+                            *d = ym[j];
+                    }
+                }
+                if (gy_hi) {
+#pragma unroll
+                    for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                        double *d = gbase + goff + RPW * st.row + j;
+                        if constexpr (CPL >= 2)
+                            *reinterpret_cast<double2 *>(d) = make_double2(yp[j], yp[j + 1]);
+                        else
+                            *d = yp[j];
+                    }
                 }
             }
             double fy[RPW + 1][CPL];
@@ -365,14 +408,29 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
                     hs[i][j] = rn_add(rn_mul(rn_sub(fx[j + 1], fx[j]), c0), rn_mul(rn_sub(fy[i + 1][j], fy[i][j]), c1));
             }
         };
-        auto fetch = [&](uint32_t q, PlaneRegs<CPL, RPW, kEarly> &P) {
+        auto fetch = [&](uint32_t q, PlaneRegs<CPL, RPW, kEarly> &P, uint32_t goff, bool centre) {
             wait_plane(q);
             const uint32_t sb = saddr(q);
             load_u(sb, P);
             if constexpr (kEarly) {
                 double(&hs)[RPW][CPL] = P.hs;
-                inplane(sb, P.u, hs);
+                inplane(sb, P.u, hs, goff, centre);
                 release(q);
+            }
+        };
+        // z ghost planes of uold (GW): the rows of the plane below the box / above it, as loaded
+        auto st_zghost = [&](const double (&v)[RPW][CPL], uint32_t goff) {
+#pragma unroll
+            for (int i = 0; i < RPW; ++i) {
+                if (!on[i]) continue;
+#pragma unroll
+                for (int j = 0; j < CPL; j += (CPL >= 2 ? 2 : 1)) {
+                    double *d = gbase + goff + i * st.row + j;
+                    if constexpr (CPL >= 2)
+                        *reinterpret_cast<double2 *>(d) = make_double2(v[i][j], v[i][j + 1]);
+                    else
+                        *d = v[i][j];
+                }
             }
         };
         {
@@ -384,7 +442,8 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) lo[i][j] = lds_f64(s0 + roff[i] + 8u * j);
-            fetch(g + 1, pa);
+            fetch(g + 1, pa, koff, true);
+            if (GW && gz_lo) st_zghost(lo, koff - pstep);
 #pragma unroll
             for (int i = 0; i < RPW; ++i)
 #pragma unroll
@@ -396,8 +455,10 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         auto plane = [&](int kk, PlaneRegs<CPL, RPW, kEarly> &cur, PlaneRegs<CPL, RPW, kEarly> &nxt) {
             const uint32_t gc = g + 1 + (uint32_t)kk;
             double hsl[RPW][CPL];  // non-early instances: the centre plane's flux sums, computed here
-            if constexpr (!kEarly) inplane(saddr(gc), cur.u, hsl);
-            fetch(gc + 1, nxt);
+            if constexpr (!kEarly) inplane(saddr(gc), cur.u, hsl, koff, true);
+            const uint32_t knext = REV ? koff - pstep : koff + pstep;
+            fetch(gc + 1, nxt, knext, kk + 1 < nk);
+            if (GW && gz_hi && kk == nk - 1) st_zghost(nxt.u, knext);
             double out[RPW][CPL];
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
@@ -739,10 +800,10 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 
 namespace {
 
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW>
 int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a,
                      int nctas, int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH>;
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH, GW>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -765,26 +826,26 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUte
     return TM_OK;
 }
 
-template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false>
+template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false, bool GW = false>
 int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a, int cpl,
                  int rows, int nctas, int ncomp, size_t smem, cudaStream_t s) {
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
-        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
     if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp
-        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
-    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV, NBRH>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
 }
 
 
@@ -938,10 +999,9 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_heat_march: bad ncomp");
     if (strides_of(L).comp >= ((int64_t)1 << 32))
         return fail(TM_ERR_INVALID, "tm_heat_march: one component of a slot must hold < 2^32 doubles");
-    const bool packed = halo_mode == TM_HALO_PACKED || halo_mode == TM_HALO_FUSED_SCATTER ||
-                        halo_mode == TM_HALO_FUSED_NBR;
-    const bool scatter = halo_mode == TM_HALO_FUSED_SCATTER || halo_mode == TM_HALO_FUSED_NBR ||
-                         halo_mode == TM_HALO_GHOSTS_XH;
+    const bool nbr_mode = halo_mode == TM_HALO_FUSED_NBR || halo_mode == TM_HALO_FUSED_NBR_GHOSTS;
+    const bool packed = halo_mode == TM_HALO_PACKED || halo_mode == TM_HALO_FUSED_SCATTER || nbr_mode;
+    const bool scatter = halo_mode == TM_HALO_FUSED_SCATTER || nbr_mode || halo_mode == TM_HALO_GHOSTS_XH;
     switch (halo_mode) {
         case TM_HALO_GHOSTS:
             if (xh_old || xh_new || d_nbr || reverse)
@@ -957,8 +1017,11 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
             break;
         case TM_HALO_FUSED_SCATTER:
         case TM_HALO_FUSED_NBR:
+        case TM_HALO_FUSED_NBR_GHOSTS:
             if (!xh_old || !xh_new || !d_nbr || xh_old == xh_new)
                 return fail(TM_ERR_INVALID, "tm_heat_march: fused modes need distinct xh_old / xh_new and d_nbr");
+            if (halo_mode == TM_HALO_FUSED_NBR_GHOSTS && (reverse || L.nghost != 1 || L.xoff < 4))
+                return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_FUSED_NBR_GHOSTS is forward, nghost 1");
             break;
         default:
             return fail(TM_ERR_INVALID, "tm_heat_march: unknown halo_mode " + std::to_string(halo_mode));
@@ -971,7 +1034,7 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
         return fail(TM_ERR_INVALID, "tm_heat_march: packed x halos need even column heights");
     // neighbour-sourced y/z halos: the column rows and the two halo rows are separate TMA boxes,
     // each landing on a stage row that must be 128-B aligned (TMA destination)
-    if (halo_mode == TM_HALO_FUSED_NBR && !(p->uniform_ny && p->max_nx % 16 == 0))
+    if (nbr_mode && !(p->uniform_ny && p->max_nx % 16 == 0))
         return fail(TM_ERR_INVALID, "tm_heat_march: TM_HALO_FUSED_NBR needs columns of one height and a width that "
                                     "is a multiple of 16");
     // A TM_HALO_FUSED_NBR step leaves the y/z face ghosts of unew unwritten; a following
@@ -999,6 +1062,7 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
     a.stage_elems = stage;
     a.xh_new = xh_new;
     a.nbr = d_nbr;
+    a.gw = const_cast<double *>(uold);  // TM_HALO_FUSED_NBR_GHOSTS only: uold's face ghosts (documented)
     const size_t smem = (size_t)kHeatStages * stage * sizeof(double) + 2 * kHeatStages * sizeof(uint64_t);
     if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_heat_march: column plane too large for shared memory");
     CUtensorMap map, xmap;
@@ -1022,12 +1086,16 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
             return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
         case TM_HALO_PACKED:
             return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+        case TM_HALO_FUSED_NBR_GHOSTS:
         case TM_HALO_FUSED_NBR: {
             CUtensorMap cmap, rmap;
             rc = encode_plane_map(&cmap, L, uold, a.box_x, p->max_ny);
             if (rc) return rc;
             rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
             if (rc) return rc;
+            if (halo_mode == TM_HALO_FUSED_NBR_GHOSTS)
+                return launch_march<true, true, false, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas,
+                                                                   ncomp_sweep, smem, s);
             if (reverse)
                 return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
                                                             smem, s);

@@ -164,15 +164,21 @@ def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None 
                                       None, None, None, 0, mf_old.stream()), "tm_heat_march")
         return
     nbr, nbr_plan = route
-    xh_new = mf_new.xh_buffer()
-    if nbr_plan is not None and mf_old.xh_current() and mf_old.ghosts_current():
-        plan, mode, xh_old = nbr_plan, _native.HALO_FUSED_NBR, mf_old._xh.data_ptr()
+    xh_new = mf_new.xh_buffer()  # not the buffer pinned as mf_new's deferred x face ghosts
+    new_ptr = mf_new.wptr
+    pending = mf_old._pending_faces
+    if nbr_plan is not None and mf_old.xh_current() and (pending is not None or mf_old.ghosts_current()):
+        plan, xh_old = nbr_plan, mf_old._xh.data_ptr()
+        # a fill_boundary deferred mf_old's y/z face ghosts: this sweep writes them as it loads them
+        mode = _native.HALO_FUSED_NBR if pending is None else _native.HALO_FUSED_NBR_GHOSTS
+        old_ptr = mf_old._data.data_ptr()  # not .ptr: that would settle the pending faces first
         _native.check(L.tm_march_plan_reset_halos(plan.handle), "tm_march_plan_reset_halos")
     else:
-        plan, mode, xh_old = march_plan(mf_old, False), _native.HALO_GHOSTS_XH, None
-    _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), mf_old.ptr, mf_new.wptr, mf_old.ncomp,
+        plan, mode, xh_old, old_ptr = march_plan(mf_old, False), _native.HALO_GHOSTS_XH, None, mf_old.ptr
+    _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), old_ptr, new_ptr, mf_old.ncomp,
                                   c[0], c[1], c[2], c[3], mode, xh_old, xh_new.data_ptr(), nbr.data_ptr(), 0,
                                   mf_old.stream()), "tm_heat_march")
+    mf_old._pending_faces = None
     mf_new._xh_key = mf_new.valid_key()
 
 
@@ -432,7 +438,7 @@ class FusedHalo:
 
         def march(plan):
             _native.check(_native.load().tm_heat_march(
-                plan.handle, old.layout.to_c(), old.ptr, new.wptr, old.ncomp, c[0], c[1], c[2], c[3], self.mode,
+                plan.handle, old.layout.to_c(), old.ptr, new.wgptr, old.ncomp, c[0], c[1], c[2], c[3], self.mode,
                 self.xh[id(old)].data_ptr(), self.xh[id(new)].data_ptr(), self.nbr.data_ptr(), int(reverse),
                 old.stream()), "tm_heat_march(fused)")
 
@@ -505,7 +511,7 @@ class FusedGSRB:
     def colour(self, color: int) -> None:
         phi, rhs = self.phi, self.rhs
         _native.check(_native.load().tm_gsrb_march(
-            self.plan.handle, phi.layout.to_c(), phi.wptr, rhs.layout.to_c(), rhs.ptr, color, self.h2,
+            self.plan.handle, phi.layout.to_c(), phi.wgptr, rhs.layout.to_c(), rhs.ptr, color, self.h2,
             self.xh.data_ptr(), self.nbr.data_ptr(), phi.stream()), "tm_gsrb_march")
 
     def sweep(self) -> None:
@@ -614,6 +620,6 @@ class SplitGSRB:
 
         phi = self.phi
         _native.check(_native.load().tm_gsrb_merge(
-            phi.layout.to_c(), phi.wptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
+            phi.layout.to_c(), phi.wgptr, self.nx, self.ny, self.nz, self.parity.data_ptr(), self.c[0].data_ptr(),
             self.c[1].data_ptr(), phi.stream()), "tm_gsrb_merge")
         fill_boundary(phi, self.geom, plan)

@@ -133,9 +133,15 @@ class DeviceFab(BoxIndexed):
         self.abox = abox
         self.ncomp = mf.ncomp
         self.slot = slot
+        self._mf = mf
         nx, ny, nz = abox.extents
         x0 = mf.layout.xoff - mf.nghost
-        self.data = mf.data[slot, :, :nz, :ny, x0:x0 + nx].permute(3, 2, 1, 0)  # (x, y, z, c)
+        self._view = mf._data[slot, :, :nz, :ny, x0:x0 + nx].permute(3, 2, 1, 0)  # (x, y, z, c)
+
+    @property
+    def data(self):
+        self._mf.settle()  # a deferred face fill is written before anyone sees the ghosts
+        return self._view
 
     def at(self, i: int, j: int, k: int, c: int = 0) -> float:
         return float(self.data[self._local(i, j, k, c)].item())
@@ -200,7 +206,15 @@ class MultiFab:
         L = self.layout
         shape = (L.nslots, ncomp, L.nz, L.ny, L.pitch)
         alloc = torch.zeros if zero else torch.empty
-        self.data = alloc(shape, dtype=torch.float64, device=self.device)
+        self._data = alloc(shape, dtype=torch.float64, device=self.device)
+        # Deferred ghosts of the reference-loop fast path (fill_boundary): y/z face ghosts the
+        # next heat_step's sweep writes, and x face ghosts kept as a snapshot of the packed x
+        # halos; written into storage ("settled") before anyone can observe them.
+        self._pending_faces = None  # copy plan of the y/z face tags
+        self._vx = None             # packed-halo snapshot holding the x face ghosts
+        self._vx_nx = 0
+        self._xh_spare = None       # second halo buffer: heat_step writes here while _xh is pinned
+        self.settles = 0            # deferred ghosts written by copy launches (diagnostic)
         self.units = []
         for u, v in enumerate(valids):
             fab = None
@@ -237,16 +251,60 @@ class MultiFab:
         return self.fab(mfi.index() if hasattr(mfi, "index") else int(mfi))
 
     @property
+    def data(self):
+        """The storage tensor ``(nslots, ncomp, nz, ny, pitch)``.  Any pending face fill is
+        written first, so every ghost a caller can observe is the reference's."""
+        self.settle()
+        return self._data
+
+    def settle(self) -> None:
+        """Write every deferred ghost (y/z faces: one copy launch; x faces: one launch from
+        the packed-halo snapshot) so the storage holds exactly a FillBoundary's ghosts."""
+        if self._pending_faces is None and self._vx is None:
+            return
+        self.settles += 1
+        self.settle_faces(count=False)
+        if self._vx is not None:
+            vx, self._vx = self._vx, None
+            _native.check(_native.load().tm_xh_to_ghosts(self.layout.to_c(), self._data.data_ptr(), vx.data_ptr(),
+                                                         self._vx_nx, _native.stream_handle(self.device)),
+                          "tm_xh_to_ghosts")
+
+    def settle_faces(self, count: bool = True) -> None:
+        """Write pending y/z face ghosts (they are copied from valid cells: before those change)."""
+        pend = self._pending_faces
+        if pend is not None:
+            self._pending_faces = None
+            self.settles += count
+            pend.run(self._data.data_ptr(), self.layout.side(), self._data.data_ptr(), self.layout.side(),
+                     _native.stream_handle(self.device))
+
+    def drop_deferred(self) -> None:
+        """A complete FillBoundary is about to rewrite every ghost the deferred ones cover."""
+        self._pending_faces = None
+        self._vx = None
+
+    @property
     def ptr(self) -> int:
         """Device address of the storage, for kernels that only READ it."""
         return self.data.data_ptr()
 
     @property
     def wptr(self) -> int:
-        """Device address for a kernel that writes valid cells (invalidates the
-        packed x halos and the filled-ghost state)."""
+        """Device address for a kernel that writes valid cells only (invalidates the
+        packed x halos and the filled-ghost state).  Deferred x face ghosts stay
+        deferred: their snapshot does not depend on the valid cells."""
+        self.settle_faces()
         self._writes += 1
-        return self.data.data_ptr()
+        return self._data.data_ptr()
+
+    @property
+    def wgptr(self) -> int:
+        """Device address for a kernel that writes (or reads) ghost cells as well as
+        valid ones: every deferred ghost is settled first."""
+        self.settle()
+        self._writes += 1
+        return self._data.data_ptr()
 
     @property
     def gptr(self) -> int:
@@ -256,16 +314,22 @@ class MultiFab:
         return self.data.data_ptr()
 
     def valid_key(self) -> tuple:
-        return (self.data._version, self._writes)
+        return (self._data._version, self._writes)
 
     def xh_buffer(self):
-        """Packed x halos of this field: (slot*ncomp+c, nz, 2, ny) over valid y/z."""
+        """Buffer a kernel writes this field's new packed x halos into:
+        (slot*ncomp+c, nz, 2, ny) over valid y/z.  While the current buffer is
+        pinned as the snapshot of deferred x face ghosts, the spare one."""
         import torch
 
+        L = self.layout
+        shape = (L.nslots * self.ncomp, L.nz - 2 * L.nghost, 2, L.ny - 2 * L.nghost)
         if self._xh is None:
-            L = self.layout
-            self._xh = torch.empty((L.nslots * self.ncomp, L.nz - 2 * L.nghost, 2, L.ny - 2 * L.nghost),
-                                   dtype=torch.float64, device=self.device)
+            self._xh = torch.empty(shape, dtype=torch.float64, device=self.device)
+        if self._vx is not None and self._vx is self._xh:
+            if self._xh_spare is None:
+                self._xh_spare = torch.empty(shape, dtype=torch.float64, device=self.device)
+            self._xh, self._xh_spare = self._xh_spare, self._xh
         return self._xh
 
     def xh_current(self) -> bool:
@@ -599,15 +663,22 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
             plan = build_fill_plan(mf, geom)
             mf._plans[("fill", geom)] = plan
     stream = mf.stream()
-    fast = _xh_fill(mf, plan) if mf.xh_current() else None
+    fast = _xh_fill(mf, plan, geom) if mf.xh_current() else None
     if fast is not None:
-        # the x faces come from the packed x halos the last heat step wrote (dense reads),
-        # every other tag from the copy kernel
-        copy, nx = fast
-        copy.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
-        _native.check(_native.load().tm_xh_to_ghosts(mf.layout.to_c(), mf.gptr, mf._xh.data_ptr(), nx, stream),
-                      "tm_xh_to_ghosts")
+        # Reference-loop fast path.  The packed x halos the last heat_step wrote are current,
+        # so the next heat_step can run the neighbour-halo march, whose y/z halo loads ARE this
+        # fill's y/z face ghosts: it writes them as it goes (TM_HALO_FUSED_NBR_GHOSTS); the x face
+        # ghosts ARE the packed halos, kept as a snapshot.  Here only the edge/corner tags run.
+        # Deferred ghosts are written before anyone can observe them (MultiFab.data / .ptr /
+        # FAB views / kernels that touch ghosts settle them), so no caller ever sees a ghost the
+        # reference would not.
+        edges, faces, nx = fast
+        mf.drop_deferred()
+        edges.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
+        mf._pending_faces = faces  # y/z faces: written by the next heat_step's sweep
+        mf._vx, mf._vx_nx = mf._xh, nx  # x faces: the packed halos of exactly this data
     else:
+        mf.drop_deferred()
         copy, halo = _device_fill(mf, plan)
         if halo is not None:
             halo.start(mf, stream)
@@ -620,33 +691,36 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
 FillBoundary = fill_boundary
 
 
-def _xh_fill(mf: MultiFab, plan: FillPlan):
-    """(copy plan of every tag except the x-face ghost columns, box width) for a
-    one-rank, one-ghost MultiFab of uniform boxes, or None.  The x faces are
-    then written by ``tm_xh_to_ghosts`` from the packed x halos."""
+def _xh_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):
+    """(copy plan of the edge/corner tags, copy plan of the y/z face tags, box width) for
+    a one-rank, one-ghost MultiFab on which heat_step runs the neighbour-halo march (the
+    fast path of the reference loop), or None.  Cached per plan and layout."""
     key = ("xh_fill",) + _plan_key(mf)
     if key in plan._device:
         return plan._device[key]
     out = None
-    widths = {mf.units[u].valid.extents for u in mf.local_units}
-    if mf.nghost == 1 and mf.dm.nranks == 1 and len(widths) == 1:
-        nx, ny, nz = next(iter(widths))
-        L = mf.layout
-        keep = []
-        covered = 0
+    from .march import xh_route
+
+    route = xh_route(mf, geom) if mf.nghost == 1 and mf.dm.nranks == 1 else None
+    L = mf.layout
+    nx = mf.units[mf.local_units[0]].valid.extents[0] if mf.local_units else 0
+    if route is not None and route[1] is not None and L.xoff >= 8 and L.xoff + nx + 8 <= L.pitch:
+        edges, yz, xfaces = [], [], 0
         for t in plan.tags:
-            v = mf.units[t.dst_unit].valid
-            d = t.dst_box
-            xface = (d.extents[0] == 1 and d.lo[0] in (v.lo[0] - 1, v.hi[0] + 1)
-                     and v.lo[1] <= d.lo[1] and d.hi[1] <= v.hi[1] and v.lo[2] <= d.lo[2] and d.hi[2] <= v.hi[2])
-            if xface:
-                covered += d.ncells
+            v, d = mf.units[t.dst_unit].valid, t.dst_box
+            out_dims = [k for k in range(3) if d.lo[k] < v.lo[k] or d.hi[k] > v.hi[k]]
+            if len(out_dims) != 1:
+                edges.append(t)
+            elif out_dims[0] == 0:
+                xfaces += d.ncells
             else:
-                keep.append(t)
-        # every x-face ghost must come from a tag (fully periodic or fully covered), or the
-        # kernel would write cells the reference leaves alone
-        if covered == 2 * ny * nz * len(mf.local_units) and (L.xoff + nx) % 2 == 0 and L.xoff + nx + 8 <= L.pitch:
-            out = (_native.CopyPlan(local_copy_tags(mf, keep), mf.ncomp), nx)
+                yz.append(t)
+        # the x faces come from the packed halos, which hold one value per row and side of
+        # every box: the plan must fill all of them (periodic / fully covered)
+        ny, nz = mf.units[mf.local_units[0]].valid.extents[1:]
+        if xfaces == 2 * ny * nz * len(mf.local_units):
+            out = (_native.CopyPlan(local_copy_tags(mf, edges), mf.ncomp),
+                   _native.CopyPlan(local_copy_tags(mf, yz), mf.ncomp), nx)
     plan._device[key] = out
     return out
 

@@ -101,7 +101,7 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
         raise ValueError("heat kernel requires nghost >= 1")
     if not mf_new.same_layout(mf_old):
         raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
-    if mf_new.data.data_ptr() == mf_old.data.data_ptr():
+    if mf_new._data.data_ptr() == mf_old._data.data_ptr():
         raise ValueError("heat_step needs distinct old/new MultiFabs (double buffering)")
     if verify and params.dt > params.stability_limit:
         warnings.warn(f"dt={params.dt} exceeds stability bound {params.stability_limit}", stacklevel=2)
@@ -174,7 +174,7 @@ def gsrb_color(phi: MultiFab, rhs: MultiFab, geom: Geometry, color: int,
     plan = schedule_sweep_plan(phi, _schedule_for(phi, schedule))
     if plan.nblocks == 0:
         return
-    _native.check(_native.load().tm_gsrb_color(plan.handle, phi.layout.to_c(), phi.wptr, rhs.layout.to_c(),
+    _native.check(_native.load().tm_gsrb_color(plan.handle, phi.layout.to_c(), phi.wgptr, rhs.layout.to_c(),
                                                rhs.ptr, color, h2, phi.stream()), "tm_gsrb_color")
 
 

@@ -202,7 +202,7 @@ class Wide4Runner:
         plan = wide4_plan(old)
         cbuf = (ctypes.c_double * 5)(c.c0, c.c1, c.c2, c.c3, c.c4)
         _native.check(_native.load().tm_wide4_march_fused(
-            plan.handle, old.layout.to_c(), old.ptr, new.wptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
+            plan.handle, old.layout.to_c(), old.ptr, new.wgptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
             dxi2[0], dxi2[1], dxi2[2], self.diffusivity * self.dt, self.nbr.data_ptr(), self.box, old.stream()),
             "tm_wide4_march_fused")
 
