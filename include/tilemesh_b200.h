@@ -251,6 +251,23 @@ int tm_wide4_march_fused(tm_march_plan *plan, const tm_layout *layout, const dou
                          int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
                          double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream);
 
+/* ---- per-tile heat operations (the reference's building blocks) -------------
+ * tm_face_flux replaces heat_flux (kernels.py:86-120 -> compiled.flux_x/y/z,
+ * compiled.py:32-63): out[f] = (u[f] - u[f - e_dir]) * dxi for the nx*ny*nz faces
+ * of a face box; `u` points at the high cell of face (0,0,0).
+ * tm_divergence_update replaces heat_divergence_update (kernels.py:122-144 ->
+ * compiled.divergence, compiled.py:66-81): on the nx*ny*nz cells of a tile,
+ * unew = uold + dtD*(((fx[+1]-fx)*dxi0 + (fy[+1]-fy)*dxi1) + (fz[+1]-fz)*dxi2)
+ * with fx/fy/fz indexed from the tile's first cell.  All arrays are strided
+ * views with x contiguous (strides of y and z in elements).  FMA-free, the
+ * reference's operation order: bit-identical. */
+int tm_face_flux(const double *u, int64_t u_sy, int64_t u_sz, int32_t direction, int32_t nx, int32_t ny,
+                 int32_t nz, double dxi, double *out, int64_t out_sy, int64_t out_sz, void *stream);
+int tm_divergence_update(double *unew, const double *uold, int64_t u_sy, int64_t u_sz, const double *fx,
+                         int64_t fx_sy, int64_t fx_sz, const double *fy, int64_t fy_sy, int64_t fy_sz,
+                         const double *fz, int64_t fz_sy, int64_t fz_sz, int32_t nx, int32_t ny, int32_t nz,
+                         double dxi0, double dxi1, double dxi2, double dtD, void *stream);
+
 /* ---- reductions (one block per unit, blocks in grid order) --------------- */
 /* d_partial[b] = serial x-fastest sum of block b (from 0.0); d_total[0] =
  * serial sum of the partials in block order: bit-identical to the

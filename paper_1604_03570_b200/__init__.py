@@ -31,6 +31,8 @@ from .stencil import (
     gsrb_solve,
     gsrb_sweep,
     heat_amplification,
+    heat_divergence_update,
+    heat_flux,
     heat_step,
     init_cosine,
     residual_maxnorm,
@@ -52,7 +54,7 @@ __all__ = [
     "DEFAULT_TILE_SIZE", "MFIter", "TileCursor", "TileSchedule", "build_schedule", "parallel_for_tiles",
     "CONTIGUOUS", "REGIONAL", "DeviceFab", "FillBoundary", "MultiFab", "fill_boundary",
     "read_plotfile", "write_plotfile",
-    "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_step", "init_cosine",
+    "HeatParams", "gsrb_color", "gsrb_solve", "gsrb_sweep", "heat_amplification", "heat_divergence_update", "heat_flux", "heat_step", "init_cosine",
     "residual_maxnorm",
     "StencilCoeffs8", "Wide4Runner", "derive_coeffs8", "wide4_amplification", "wide4_stable_dt",
     "wide4_step",

@@ -50,7 +50,7 @@ EXPORTS = [
     "tm_residual_maxnorm", "tm_reduce_sum", "tm_reduce_minmax",
     "tm_march_plan_create", "tm_march_plan_destroy", "tm_march_plan_reset_halos", "tm_heat_march", "tm_gsrb_march", "tm_wide4_march",
     "tm_wide4_march_fused",
-    "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass",
+    "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass", "tm_face_flux", "tm_divergence_update",
     "tm_comm_nccl_version", "tm_comm_unique_id", "tm_comm_create", "tm_comm_destroy",
     "tm_exchange_create", "tm_exchange_destroy", "tm_halo_exchange",
 ]
@@ -104,6 +104,9 @@ def load():
     L.tm_gsrb_split.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, P(tm_layout), vp, vp, vp, vp]
     L.tm_gsrb_merge.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, vp]
     L.tm_gsrb_split_pass.argtypes = [vp, i32, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp]
+    L.tm_face_flux.argtypes = [vp, i64, i64, i32, i32, i32, i32, f64, vp, i64, i64, vp]
+    L.tm_divergence_update.argtypes = [vp, vp, i64, i64, vp, i64, i64, vp, i64, i64, vp, i64, i64, i32, i32, i32,
+                                       f64, f64, f64, f64, vp]
     L.tm_comm_nccl_version.argtypes = [P(i32)]
     L.tm_comm_unique_id.argtypes = [ctypes.c_char_p]
     L.tm_comm_create.argtypes = [ctypes.c_char_p, i32, i32, P(vp)]

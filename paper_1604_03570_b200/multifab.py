@@ -676,7 +676,14 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
         mf.drop_deferred()
         edges.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
         mf._pending_faces = faces  # y/z faces: written by the next heat_step's sweep
-        mf._vx, mf._vx_nx = mf._xh, nx  # x faces: the packed halos of exactly this data
+        if _capturing() and not _SNAPSHOTS_IN_CAPTURE[0]:
+            # a CUDA graph freezes buffer pointers, and pinning the halo buffer as a snapshot
+            # makes the next heat_step write the other one: the pattern repeats only every two
+            # steps per field.  Unknown captures get the x faces written now instead.
+            _native.check(_native.load().tm_xh_to_ghosts(mf.layout.to_c(), mf._data.data_ptr(),
+                                                         mf._xh.data_ptr(), nx, stream), "tm_xh_to_ghosts")
+        else:
+            mf._vx, mf._vx_nx = mf._xh, nx  # x faces: the packed halos of exactly this data
     else:
         mf.drop_deferred()
         copy, halo = _device_fill(mf, plan)
@@ -689,6 +696,29 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
 
 
 FillBoundary = fill_boundary
+
+
+_SNAPSHOTS_IN_CAPTURE = [False]
+
+
+def _capturing() -> bool:
+    import torch
+
+    return torch.cuda.is_current_stream_capturing()
+
+
+class snapshots_in_capture:
+    """Context: the CUDA graph being captured replays a whole number of pairs of
+    reference-loop steps per field (runner.HeatRunner's unfused 4-step graphs),
+    so pinned packed-halo snapshots (fill_boundary's deferred x faces) repeat
+    with the graph and may be used."""
+
+    def __enter__(self):
+        _SNAPSHOTS_IN_CAPTURE[0] = True
+        return self
+
+    def __exit__(self, *exc):
+        _SNAPSHOTS_IN_CAPTURE[0] = False
 
 
 def _xh_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):

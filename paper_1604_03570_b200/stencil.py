@@ -120,6 +120,75 @@ def heat_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, params: HeatPa
                                   dxi0, dxi1, dxi2, dtD, mf_old.stream()), "tm_heat_sweep")
 
 
+def _strides3(t, what: str):
+    """(y, z) element strides of a device 3-D view with x contiguous."""
+    if t.dim() < 3 or t.stride(0) != 1:
+        raise ValueError(f"{what} must be a device array with x contiguous")
+    return t.stride(1), t.stride(2)
+
+
+def heat_flux(u, face_box, direction: int, dx: float, out=None):
+    """F(face) = (u(high cell) - u(low cell)) / dx for every face in ``face_box``
+    (reference kernels.py:86-120) on a device FAB; returns a device array shaped
+    like the face box (x fastest, like the reference's F-order array)."""
+    import torch
+
+    from .box import Box
+
+    if not face_box.itype[direction]:
+        raise ValueError(f"face box must be node-centered in direction {direction}")
+    cells = Box(tuple(lo - (1 if d == direction else 0) for d, lo in enumerate(face_box.lo)), face_box.hi)
+    if not u.abox.contains(cells):
+        raise ValueError(f"flux on {face_box} needs cells {cells}; fab only covers {u.abox}"
+                         " (at least one filled ghost cell is required)")
+    ex = face_box.extents
+    view = u.data
+    if out is None:
+        out = torch.empty(tuple(reversed(ex)), dtype=torch.float64, device=view.device).permute(2, 1, 0)
+    elif tuple(out.shape) != tuple(ex):
+        raise ValueError(f"out has shape {tuple(out.shape)}, face box needs {tuple(ex)}")
+    if any(e == 0 for e in ex):
+        return out
+    lo = u.abox.lo
+    hi_cell = view[face_box.lo[0] - lo[0], face_box.lo[1] - lo[1], face_box.lo[2] - lo[2], 0]
+    su = _strides3(view[..., 0], "u")
+    so = _strides3(out, "out")
+    _native.check(_native.load().tm_face_flux(hi_cell.data_ptr(), su[0], su[1], direction, ex[0], ex[1], ex[2],
+                                              1.0 / dx, out.data_ptr(), so[0], so[1],
+                                              _native.stream_handle(view.device)), "tm_face_flux")
+    return out
+
+
+def heat_divergence_update(u_new, u_old, fluxes, tile, params: HeatParams) -> None:
+    """u_new = u_old + dt*D*div(F) on every cell of the tile (reference
+    kernels.py:122-144); the flux arrays are indexed from tile.lo (heat_flux's
+    output for the tile's three face boxes)."""
+    fx, fy, fz = fluxes
+    if u_new.abox.lo != u_old.abox.lo:
+        raise ValueError("u_new and u_old must share an allocation box")
+    e = tile.extents
+    for f, d in ((fx, 0), (fy, 1), (fz, 2)):
+        need = tuple(e[k] + (1 if k == d else 0) for k in range(3))
+        if tuple(f.shape[:3]) != need:
+            raise ValueError(f"flux {'xyz'[d]} has shape {tuple(f.shape)}, tile needs {need}")
+    if any(v == 0 for v in e):
+        return
+    dxi = tuple(1.0 / d for d in params.dx)
+    lo = u_old.abox.lo
+    at = tuple(tile.lo[k] - lo[k] for k in range(3))
+    vn, vo = u_new.data, u_old.data
+    su = _strides3(vo[..., 0], "u_old")
+    if _strides3(vn[..., 0], "u_new") != su:
+        raise ValueError("u_new and u_old must have the same layout")
+    sx, sy, sz = (_strides3(f, "flux") for f in fluxes)
+    u_new._mf.wptr  # noqa: B018 -- a library kernel writes u_new's valid cells (state keys)
+    _native.check(_native.load().tm_divergence_update(
+        vn[at[0], at[1], at[2], 0].data_ptr(), vo[at[0], at[1], at[2], 0].data_ptr(), su[0], su[1],
+        fx.data_ptr(), sx[0], sx[1], fy.data_ptr(), sy[0], sy[1], fz.data_ptr(), sz[0], sz[1], e[0], e[1], e[2],
+        dxi[0], dxi[1], dxi[2], params.diffusivity * params.dt, _native.stream_handle(vo.device)),
+        "tm_divergence_update")
+
+
 def heat_sweep_plan(mf_new: MultiFab, mf_old: MultiFab, params: HeatParams, plan) -> None:
     """Kernel A over an explicit block table (e.g. the interior or boundary
     half of an overlapped step).  No checks: internal helper."""

@@ -12,6 +12,7 @@ import torch  # noqa: E402
 
 import paper_1604_03570_b200 as tm  # noqa: E402
 from paper_1604_03570_b200.multifab import _xh_fill  # noqa: E402
+from paper_1604_03570_b200.runner import HeatRunner  # noqa: E402
 from tools.sweep_shapes import graph_time  # noqa: E402
 
 
@@ -49,11 +50,31 @@ def main():
     res = {"edge/corner copies (the fill on the loop's path)": graph_time(edge_part, 20),
            "y/z face copies (settling deferred faces)": graph_time(face_part, 20)}
     a._xh_key = a.valid_key()  # the timing loops above do not change valid cells
-    res["loop step (fill + heat_step)"] = graph_time(pair, 10) / 2
+    # the loop as a drop-in caller issues it (eager Python), and as HeatRunner(fused=False)
+    # replays it (4-step graphs: the packed-halo buffers repeat every two steps per field)
+    for _ in range(2):
+        pair()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(20):
+        pair()
+    e1.record()
+    torch.cuda.synchronize()
+    res["loop step, eager Python"] = e0.elapsed_time(e1) / 40
+    r = HeatRunner(a, geom, p, None, plan, fused=False)
+    r.advance(8)
+    torch.cuda.synchronize()
+    e0.record()
+    r.advance(40, finalize=False)
+    e1.record()
+    torch.cuda.synchronize()
+    res["loop step (fill + heat_step)"] = e0.elapsed_time(e1) / 40
     for k, ms in res.items():
         print(f"{cfg} {k}: {ms * 1e3:.1f} us")
     step = res["loop step (fill + heat_step)"]
-    print(f"{cfg} reference loop: {cells / step / 1e6:.1f} G cell-upd/s, {16 * cells / step / 1e6 / 6553.6:.3f} of 6553.6 GB/s")
+    print(f"{cfg} reference loop (HeatRunner graph): {cells / step / 1e6:.1f} G cell-upd/s, "
+          f"{16 * cells / step / 1e6 / 6553.6:.3f} of 6553.6 GB/s")
 
 
 if __name__ == "__main__":
