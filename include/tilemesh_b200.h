@@ -231,7 +231,8 @@ int tm_gsrb_split_pass(tm_march_plan *plan, int32_t nslots, int32_t nx, int32_t 
  * Replaces compiled.wide4_tiles / wide4_range (compiled.py:102-141) as driven
  * by kernels.wide4_step (kernels.py:218-247) and the reference's loop variant
  * (kernels.py:309-342), over every column of a march plan (columns of the
- * full box width <= 128, <= 16 rows (<= 8 when wider than 64), full z).
+ * full box width <= 128, <= 16 rows (<= 8 when wider than 64), full z; or, on
+ * Kernel W2, widths <= 64 with row counts that are multiples of 4, <= 32).
  * coeffs5 = host array {c0, c1, c2, c3, c4} (StencilCoeffs8); dxi2_d = 1/dx_d^2;
  * dtD = D*dt.  Needs nghost >= 4 with filled ghosts (FillBoundary).  Per cell,
  * in the reference's operation order, FMA-free: bit-identical. */
@@ -250,6 +251,18 @@ int tm_wide4_march(tm_march_plan *plan, const tm_layout *layout, const double *u
 int tm_wide4_march_fused(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                          int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
                          double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream);
+/* The reference step loop's pair (fill_boundary, level.py:297-323 + wide4_step,
+ * kernels.py:218-247) as ONE launch that writes nothing but unew's valid cells:
+ * every x/y/z halo (4 deep) is read straight from the face neighbour's valid
+ * cells of uold -- the values a FillBoundary would have copied -- so neither
+ * field's ghosts are read or written (faces with no neighbour, d_nbr < 0, read
+ * uold's own ghosts).  Needs uniform boxes whose width is a multiple of 4 and
+ * <= 64, cut into full-width columns of one height (a multiple of 4, <= 32,
+ * dividing the box height); each box extent >= 4.  Kernel W2 (tm_wide4.cu).
+ * tm_wide4_march runs W2 too (halos from ghosts) when its plan allows. */
+int tm_wide4_march_nbr(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                       double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream);
 
 /* ---- per-tile heat operations (the reference's building blocks) -------------
  * tm_face_flux replaces heat_flux (kernels.py:86-120 -> compiled.flux_x/y/z,

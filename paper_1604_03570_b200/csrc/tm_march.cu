@@ -948,7 +948,13 @@ int tm_march_plan_create(const tm_block *cols, int64_t ncols, int32_t nctas, tm_
     p->max_nx = mx;
     p->max_ny = my;
     p->even = even;
-    for (int64_t c = 0; c < ncols; ++c) p->uniform_ny = p->uniform_ny && cols[c].ny == my;
+    p->x0_common = ncols ? cols[0].x0 : -1;
+    for (int64_t c = 0; c < ncols; ++c) {
+        p->uniform_ny = p->uniform_ny && cols[c].ny == my;
+        p->uniform_nx = p->uniform_nx && cols[c].nx == mx;
+        p->ny_mult4 = p->ny_mult4 && cols[c].ny % 4 == 0;
+        if (cols[c].x0 != p->x0_common) p->x0_common = -1;
+    }
     cudaError_t e = cudaMalloc(&p->d_cols, sizeof(tm_block) * std::max<int64_t>(ncols, 1));
     if (e == cudaSuccess) e = cudaMalloc(&p->d_segs, sizeof(Segment) * std::max<size_t>(segs.size(), 1));
     if (e == cudaSuccess) e = cudaMalloc(&p->d_seg_begin, sizeof(int32_t) * (nctas + 1));

@@ -23,6 +23,9 @@ struct tm_march_plan {
     int max_nx = 0, max_ny = 0;
     bool even = true;
     bool uniform_ny = true;  // every column has max_ny rows
+    bool uniform_nx = true;  // every column has max_nx cells per row
+    bool ny_mult4 = true;    // every column's row count is a multiple of 4 (Kernel W2 row groups)
+    int32_t x0_common = -1;  // the x0 every column starts at, or -1
     int32_t last_halo_mode = -1;          // mode of the last fused tm_heat_march (tm_march_plan_reset_halos)
     const void *last_xh_new = nullptr;    // and the packed x halo it wrote
 };

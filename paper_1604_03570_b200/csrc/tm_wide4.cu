@@ -300,6 +300,380 @@ int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int nco
     return TM_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Kernel W2: the same step on columns of up to 32 rows (full box width <= 64).
+//
+// Why: Kernel W's 16-row columns re-read 8 halo rows per 16 (1.5x in y), and its
+// fused variant scatters every cell within 4 of a face into the neighbours' ghost
+// layers -- 8-B and 32-B partial-sector writes that HBM's ECC turns into
+// read-modify-writes (ncu r01: 363 MB read for 273 MB requested).  W2 halves
+// the y re-reads (8 per 32 rows) and, in NBR mode, reads every face halo
+// straight from the face neighbour's valid cells, so a fused step writes nothing
+// but unew's valid cells.
+//
+// Work: 8 consumer warps; warp w owns rows 4w .. 4w+3 of the column, lane l the
+// cell pair (2l, 2l+1) of each row.  The z window (planes k-4 .. k+4 of the
+// warp's 8 cells) lives in registers and shifts by one plane per step.  A plane's stage stays resident
+// from landing until it is the centre plane (its x/y neighbours), then is
+// released; window-only planes (the 4 below / above a segment) are released on
+// landing.
+//
+// Stage layout (doubles), bw = stage row width:
+//   GHOST (tm_wide4_march, ghosts filled by FillBoundary): one TMA box
+//          (nx+8) x (R+8) at (x0-4, y0-4): rows -4 .. R+3, columns -4 .. nx+3.
+//   NBR (tm_wide4_march_nbr): rows -4..-1 (4 x nx) | column rows 0..R-1 (R x nx) |
+//          rows R..R+3 (4 x nx), then the x halos XL (R x 4) and XH (R x 4), each
+//          region 128-B aligned (TMA destination); halo rows/columns/planes come
+//          from the face neighbour's valid cells (own ghosts where there is none).
+// ---------------------------------------------------------------------------
+#ifndef TM_W2_NW
+#define TM_W2_NW 8
+#endif
+constexpr int kW2Warps = TM_W2_NW;     // consumer warps
+constexpr int kW2Rows = 32 / TM_W2_NW;  // rows per consumer warp
+
+struct W2Args {
+    const tm_block *cols;
+    const Segment *segs;
+    const int32_t *seg_begin;
+    double *out;
+    tm_layout L;
+    double c0, c1, c2, c3, c4;
+    double d0, d1, d2, dtD;
+    int32_t bw;                      // stage row width (doubles)
+    int32_t stage_elems, off_xl, off_xh;
+    uint32_t tx_c, tx_h;             // TMA bytes of a centre plane / a window-only plane
+    const int32_t *nbr;              // NBR: face neighbours per slot
+    int32_t nxv, nyv, nzv;           // NBR: uniform box extents
+};
+
+// A CTA's segments as the producer lane needs them, staged in shared memory at kernel
+// start (segments past kW2SegCache are read from global memory): dependent global loads
+// on the issue path cost ~10 us per C2-shaped step when consumers issued (r02).
+constexpr int kW2SegCache = 32;
+struct W2Seg {
+    int32_t slot, x0, y0, z0, ny, k0, nk, base;  // base: CTA plane counter of the segment's first plane
+    int32_t nb[6];                               // face neighbours (NBR)
+    int32_t pad[2];
+};
+static_assert(sizeof(W2Seg) == 64, "W2Seg is four 16-B words");
+
+template <bool NBR>
+__device__ __forceinline__ W2Seg w2_seg_global(const W2Args &A, int s, uint32_t base) {
+    const tmk::Segment sg = A.segs[s];
+    const tm_block c = A.cols[sg.col];
+    W2Seg d;
+    d.slot = c.slot;
+    d.x0 = c.x0;
+    d.y0 = c.y0;
+    d.z0 = c.z0;
+    d.ny = c.ny;
+    d.k0 = sg.k0;
+    d.nk = sg.k1 - sg.k0;
+    d.base = (int32_t)base;
+#pragma unroll
+    for (int f = 0; f < 6; ++f) d.nb[f] = NBR ? A.nbr[6 * c.slot + f] : -1;
+    d.pad[0] = d.pad[1] = 0;
+    return d;
+}
+
+// Issue CTA plane P of a W2 launch into its stage.  `cur` = the producer's forward cursor
+// (segment index relative to the CTA's first, and that segment's first CTA plane).
+template <bool NBR>
+__device__ __forceinline__ void w2_issue(const W2Args &A, const CUtensorMap *cmap, const CUtensorMap *ymap,
+                                         const CUtensorMap *xmap, double *stages, uint64_t *bars,
+                                         const W2Seg *cache, int s_begin, int s_end, int32_t *cur, uint32_t P,
+                                         int comp) {
+    using namespace tmk;
+    const int nc = A.L.ncomp, ng = A.L.nghost;
+    int i = *cur;
+    W2Seg d = i < kW2SegCache ? cache[i] : w2_seg_global<NBR>(A, s_begin + i, 0);
+    uint32_t base = i < kW2SegCache ? (uint32_t)d.base : (uint32_t)cur[1];
+    while (P >= base + (uint32_t)(d.nk + 2 * kR) && s_begin + i + 1 < s_end) {
+        base += (uint32_t)(d.nk + 2 * kR);
+        ++i;
+        d = i < kW2SegCache ? cache[i] : w2_seg_global<NBR>(A, s_begin + i, base);
+    }
+    cur[0] = i;
+    cur[1] = (int32_t)base;
+    const int q = (int)(P - base);
+    const int k = d.k0 - kR + q;  // valid plane index
+    const int w = d.slot * nc + comp;
+    double *stg = stages + (P & (kW4Stages - 1)) * A.stage_elems;
+    uint64_t *bar = &bars[P & (kW4Stages - 1)];
+    fence_proxy_async_shared();  // generic reads of the stage's last plane before the async overwrite
+    if (NBR) {
+        int ws = d.slot, zs = d.z0 + k;
+        if (k < 0 && d.nb[4] >= 0) {
+            ws = d.nb[4];
+            zs += A.nzv;
+        } else if (k >= A.nzv && d.nb[5] >= 0) {
+            ws = d.nb[5];
+            zs -= A.nzv;
+        }
+        const bool centre = q >= kR && q < d.nk + kR;  // always a plane of our own box
+        mbar_arrive_expect_tx(bar, centre ? A.tx_c : A.tx_h);
+        tma_load_plane(stg + kR * A.bw, cmap, bar, d.x0, d.y0, zs, ws * nc + comp);
+        if (centre) {
+            if (d.y0 - ng == 0 && d.nb[2] >= 0)
+                tma_load_plane(stg, ymap, bar, d.x0, d.y0 - kR + A.nyv, zs, d.nb[2] * nc + comp);
+            else
+                tma_load_plane(stg, ymap, bar, d.x0, d.y0 - kR, zs, w);
+            double *yh = stg + (kR + d.ny) * A.bw;
+            if (d.y0 - ng + d.ny == A.nyv && d.nb[3] >= 0)
+                tma_load_plane(yh, ymap, bar, d.x0, d.y0 + d.ny - A.nyv, zs, d.nb[3] * nc + comp);
+            else
+                tma_load_plane(yh, ymap, bar, d.x0, d.y0 + d.ny, zs, w);
+            if (d.nb[0] >= 0)
+                tma_load_plane(stg + A.off_xl, xmap, bar, d.x0 + A.nxv - kR, d.y0, zs, d.nb[0] * nc + comp);
+            else
+                tma_load_plane(stg + A.off_xl, xmap, bar, d.x0 - kR, d.y0, zs, w);
+            if (d.nb[1] >= 0)
+                tma_load_plane(stg + A.off_xh, xmap, bar, d.x0, d.y0, zs, d.nb[1] * nc + comp);
+            else
+                tma_load_plane(stg + A.off_xh, xmap, bar, d.x0 + A.nxv, d.y0, zs, w);
+        }
+    } else {
+        mbar_arrive_expect_tx(bar, A.tx_c);
+        tma_load_plane(stg, cmap, bar, d.x0 - kR, d.y0 - kR, d.z0 + k, w);
+    }
+}
+
+// Warp specialisation with register rebalancing: a 9th (producer) warp would put 3 warps on
+// one SM sub-partition and cap every thread at 168 registers, but the consumers' window
+// alone takes 144.  So the block is three warpgroups: warpgroup 2 is the producer (one
+// lane issues every TMA load; setmaxnreg.dec to 40 registers), warpgroups 0-1 are the
+// 8 consumer warps (setmaxnreg.inc to 232).  An earlier producer-less variant (the warp
+// releasing a stage last issued its refill) put the issue latency on the slowest warp's
+// critical path: 95 vs this kernel's time on the fused C2-shaped step (profiles/r02).
+constexpr int kW2ProdRegs = 40, kW2ConsRegs = 232;
+
+template <bool NBR>
+__global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
+    wide4_col_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap ymap,
+                     const __grid_constant__ CUtensorMap xmap, W2Args a) {
+    using namespace tmk;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // TMA destinations must be 128-B aligned; the static shared arrays below precede the
+    // dynamic window, so align explicitly (the launch adds 128 B of slack)
+    unsigned char *smem_al = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
+    double *stages = reinterpret_cast<double *>(smem_al);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_al + (size_t)kW4Stages * a.stage_elems * sizeof(double));
+    uint64_t *empty = bars + kW4Stages;
+    __shared__ __align__(16) W2Seg seg_cache[kW2SegCache];  // the CTA's first segments
+
+    const int comp = blockIdx.y;
+    const int s_begin = a.seg_begin[blockIdx.x], s_end = a.seg_begin[blockIdx.x + 1];
+    if (s_begin >= s_end) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    if (tid == 0) {
+        prefetch_tensormap(&cmap);
+        if (NBR) {
+            prefetch_tensormap(&ymap);
+            prefetch_tensormap(&xmap);
+        }
+#pragma unroll
+        for (int s = 0; s < kW4Stages; ++s) {
+            mbar_init(&bars[s], 1);
+            mbar_init(&empty[s], kW2Warps);
+        }
+        fence_mbar_init();
+        uint32_t base = 0;
+        for (int i = 0; i < kW2SegCache && s_begin + i < s_end; ++i) {
+            seg_cache[i] = w2_seg_global<NBR>(a, s_begin + i, base);
+            base += (uint32_t)(seg_cache[i].nk + 2 * kR);
+        }
+    }
+    grid_dep_launch();
+    __syncthreads();
+    grid_dep_wait();  // previous step complete: its unew is our uold (and vice versa)
+
+    if (warp >= kW2Warps) {  // ---------------- producer warpgroup ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kW2ProdRegs));
+        if (warp == kW2Warps && lane == 0) {
+            uint32_t total = 0;
+            for (int s = s_begin; s < s_end; ++s) total += (uint32_t)(a.segs[s].k1 - a.segs[s].k0 + 2 * kR);
+            int32_t cur[2] = {0, 0};
+            for (uint32_t P = 0; P < total; ++P) {
+                if (P >= (uint32_t)kW4Stages) mbar_wait(&empty[P & (kW4Stages - 1)], ((P / kW4Stages) - 1) & 1);
+                w2_issue<NBR>(a, &cmap, &ymap, &xmap, stages, bars, seg_cache, s_begin, s_end, cur, P, comp);
+            }
+        }
+        return;
+    }
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kW2ConsRegs));
+
+    // ---------------- consumer warps ----------------
+    const uint32_t sbase = smem_u32(stages);
+    const uint32_t bfull = smem_u32(bars), bempty = smem_u32(empty);
+    const uint32_t sbytes = (uint32_t)a.stage_elems * 8u;
+    auto saddr = [&](uint32_t q) { return sbase + (q & (kW4Stages - 1)) * sbytes; };
+    auto wait_plane = [&](uint32_t q) { mbar_wait_u32(bfull + (q & (kW4Stages - 1)) * 8u, (q / kW4Stages) & 1u); };
+    auto release = [&](uint32_t q) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive_u32(bempty + (q & (kW4Stages - 1)) * 8u);
+    };
+    const Strides st = strides_of(a.L);
+    const double c0 = a.c0, d0 = a.d0, d1 = a.d1, d2 = a.d2, dtD = a.dtD;
+    const double cm[kR + 1] = {a.c0, a.c1, a.c2, a.c3, a.c4};
+    const int RS = a.bw * 8;  // stage row stride in bytes
+    const uint32_t pstep = (uint32_t)st.plane;
+    const int r0 = warp * kW2Rows;
+    uint32_t g = 0;
+
+    for (int s = s_begin; s < s_end; ++s) {
+        const Segment sg = a.segs[s];
+        const tm_block c = a.cols[sg.col];
+        const int nk = sg.k1 - sg.k0;
+        const bool wact = r0 < c.ny;  // rows come in groups of 4 (host-checked)
+        const int cx = min(2 * lane, c.nx - 2);
+        const bool on = wact && 2 * lane < c.nx;
+        // byte offsets inside a stage: the warp's first row at this lane's first cell, and the
+        // x pairs q = 0..4 (columns cx-4+2q) at that row, with their row strides
+        const int rowb = ((r0 + kR) * a.bw + (NBR ? 0 : kR) + cx) * 8;
+        int xo[2 * kR / 2 + 1], xs[2 * kR / 2 + 1];
+#pragma unroll
+        for (int q = 0; q <= kR; ++q) {
+            const int cq = cx - kR + 2 * q;
+            if (NBR && cq < 0) {
+                xo[q] = (a.off_xl + r0 * kR + cq + kR) * 8;
+                xs[q] = kR * 8;
+            } else if (NBR && cq >= c.nx) {
+                xo[q] = (a.off_xh + r0 * kR + cq - c.nx) * 8;
+                xs[q] = kR * 8;
+            } else {
+                xo[q] = rowb + (cq - cx) * 8;
+                xs[q] = RS;
+            }
+        }
+        double *const orow =
+            a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)(c.y0 + r0) * st.row + c.x0 + cx;
+        uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane);
+
+        double w[2 * kR + 1][kW2Rows][2];  // window slot (q % 9) <- segment plane q
+        auto load_rows = [&](uint32_t sb, double (&dst)[kW2Rows][2]) {
+#pragma unroll
+            for (int i = 0; i < kW2Rows; ++i) lds_f64x2(sb + (uint32_t)(rowb + i * RS), dst[i][0], dst[i][1]);
+        };
+        // priming: segment planes 0..7 (k0-4 .. k0+3)
+#pragma unroll
+        for (int q = 0; q < 2 * kR; ++q) {
+            wait_plane(g + q);
+            if (wact) load_rows(saddr(g + q), w[q]);
+            if (q < kR || q >= nk + kR) release(g + q);  // never a centre plane
+        }
+        auto body = [&](int kk) {
+            constexpr int ROT = 0;  // window slot m holds plane k-4+m (shifted after each plane)
+            constexpr int CEN = (ROT + kR) % (2 * kR + 1);
+            const uint32_t qn = g + (uint32_t)kk + 2 * kR;  // leading edge: plane k+4
+            wait_plane(qn);
+            if (wact) load_rows(saddr(qn), w[(ROT + 2 * kR) % (2 * kR + 1)]);
+            if (kk + 2 * kR >= nk + kR) release(qn);  // window-only plane
+            const uint32_t qc = g + (uint32_t)kk + kR;
+            const uint32_t sc = saddr(qc);
+            if (wact) {
+#pragma unroll
+                for (int i = 0; i < kW2Rows; ++i) {
+                    double v[2 * kR + 2];  // columns cx-4 .. cx+5 of row i
+#pragma unroll
+                    for (int q = 0; q <= kR; ++q) {
+                        if (q == kR / 2) {
+                            v[2 * q] = w[CEN][i][0];
+                            v[2 * q + 1] = w[CEN][i][1];
+                        } else {
+                            lds_f64x2(sc + (uint32_t)(xo[q] + i * xs[q]), v[2 * q], v[2 * q + 1]);
+                        }
+                    }
+                    double sx[2], sy[2], sz[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const double cu = rn_mul(c0, w[CEN][i][j]);
+                        sx[j] = cu;
+                        sy[j] = cu;
+                        sz[j] = cu;
+                    }
+#pragma unroll
+                    for (int m = 1; m <= kR; ++m) {
+                        double ym[2], yp[2];
+                        if (i - m >= 0) {
+                            ym[0] = w[CEN][i - m][0];
+                            ym[1] = w[CEN][i - m][1];
+                        } else {
+                            lds_f64x2(sc + (uint32_t)(rowb + (i - m) * RS), ym[0], ym[1]);
+                        }
+                        if (i + m < kW2Rows) {
+                            yp[0] = w[CEN][i + m][0];
+                            yp[1] = w[CEN][i + m][1];
+                        } else {
+                            lds_f64x2(sc + (uint32_t)(rowb + (i + m) * RS), yp[0], yp[1]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            sx[j] = rn_add(sx[j], rn_mul(cm[m], rn_add(v[kR + j - m], v[kR + j + m])));
+                            sy[j] = rn_add(sy[j], rn_mul(cm[m], rn_add(ym[j], yp[j])));
+                            sz[j] = rn_add(sz[j], rn_mul(cm[m], rn_add(w[(ROT + kR - m) % (2 * kR + 1)][i][j],
+                                                                        w[(ROT + kR + m) % (2 * kR + 1)][i][j])));
+                        }
+                    }
+                    double out[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const double lap = rn_add(rn_add(rn_mul(sx[j], d0), rn_mul(sy[j], d1)), rn_mul(sz[j], d2));
+                        out[j] = rn_add(w[CEN][i][j], rn_mul(dtD, lap));
+                    }
+                    if (on) *reinterpret_cast<double2 *>(orow + (int64_t)i * st.row + koff) = make_double2(out[0], out[1]);
+                }
+            }
+            release(qc);
+            koff += pstep;
+#pragma unroll
+            for (int m = 0; m < 2 * kR; ++m)
+#pragma unroll
+                for (int i = 0; i < kW2Rows; ++i) {
+                    w[m][i][0] = w[m + 1][i][0];
+                    w[m][i][1] = w[m + 1][i][1];
+                }
+        };
+        // (Renaming the window slots instead of shifting them needs the plane loop unrolled
+        // nine times; that code no longer fits the instruction cache: ncu r02, 'no
+        // instructions' the top stall.)
+        for (int kk = 0; kk < nk; ++kk) body(kk);
+        g += nk + 2 * kR;
+    }
+}
+
+template <bool NBR>
+int launch_w2(const CUtensorMap &cmap, const CUtensorMap &ymap, const CUtensorMap &xmap, const W2Args &a, int nctas,
+              int ncomp, size_t smem, cudaStream_t s) {
+    auto kern = wide4_col_kernel<NBR>;
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+        if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(wide4 W2)");
+        configured = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nctas, ncomp);
+    cfg.blockDim = dim3((kW2Warps + 4) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, cmap, ymap, xmap, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return tmk::cuda_fail(e, "wide4 W2 launch");
+    return TM_OK;
+}
+
+// Kernel W2 takes plans of columns <= 64 wide (even) whose row counts are multiples of 4, <= 32.
+bool w2_eligible(const tm_march_plan *p) {
+    return p->even && p->max_nx <= 64 && p->ny_mult4 && p->max_ny <= kW2Warps * kW2Rows;
+}
+
 }  // namespace
 
 namespace {
@@ -313,6 +687,59 @@ int wide4_dispatch(const CUtensorMap &map, const W4Args &a, const tm_march_plan 
     if (cpl == 2) return launch_wide4_one<2, 16, false, SCATTER>(map, a, p->nctas, ncomp, smem, s);
     if (p->max_ny > 8) return tmk::fail(TM_ERR_INVALID, "tm_wide4_march: columns wider than 64 must be <= 8 rows");
     return launch_wide4_one<4, 8, false, SCATTER>(map, a, p->nctas, ncomp, smem, s);
+}
+
+// Kernel W2 launch: GHOST (x/y/z halos from uold's ghost cells) or NBR (from the face
+// neighbours' valid cells, d_box = uniform box extents).  `base` carries the coefficients.
+template <bool NBR>
+int w2_common(const tm_march_plan *p, const tm_layout &L, const double *uold, const W4Args &base, int ncomp_sweep,
+              const int32_t *d_box, cudaStream_t s) {
+    using namespace tmk;
+    W2Args a{};
+    a.cols = p->d_cols;
+    a.segs = p->d_segs;
+    a.seg_begin = p->d_seg_begin;
+    a.out = base.out;
+    a.L = L;
+    a.c0 = base.c0;
+    a.c1 = base.c1;
+    a.c2 = base.c2;
+    a.c3 = base.c3;
+    a.c4 = base.c4;
+    a.d0 = base.d0;
+    a.d1 = base.d1;
+    a.d2 = base.d2;
+    a.dtD = base.dtD;
+    const int nx = p->max_nx, R = p->max_ny;
+    CUtensorMap cmap, ymap, xmap;
+    int rc;
+    if (NBR) {
+        a.bw = nx;
+        a.off_xl = ((nx * (R + 2 * kR) + 15) / 16) * 16;
+        a.off_xh = a.off_xl + ((kR * R + 15) / 16) * 16;
+        a.stage_elems = a.off_xh + ((kR * R + 15) / 16) * 16;
+        a.tx_c = (uint32_t)((nx * R + 2 * kR * nx + 2 * kR * R) * 8);
+        a.tx_h = (uint32_t)(nx * R * 8);
+        a.nbr = base.nbr;
+        a.nxv = d_box[0];
+        a.nyv = d_box[1];
+        a.nzv = d_box[2];
+        rc = encode_plane_map(&cmap, L, uold, nx, R);
+        if (!rc) rc = encode_plane_map(&ymap, L, uold, nx, kR);
+        if (!rc) rc = encode_plane_map(&xmap, L, uold, kR, R);
+    } else {
+        a.bw = nx + 2 * kR;
+        a.stage_elems = ((a.bw * (R + 2 * kR) + 15) / 16) * 16;
+        a.tx_c = a.tx_h = (uint32_t)(a.bw * (R + 2 * kR) * 8);
+        a.nyv = L.ny - 2 * L.nghost;
+        rc = encode_plane_map(&cmap, L, uold, a.bw, R + 2 * kR);
+        ymap = xmap = cmap;
+    }
+    if (rc) return rc;
+    // stages + full barriers + release counters + 128 B of alignment slack
+    const size_t smem = (size_t)kW4Stages * a.stage_elems * sizeof(double) + 2 * kW4Stages * sizeof(uint64_t) + 128;
+    if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "wide4 W2: column plane too large for shared memory");
+    return launch_w2<NBR>(cmap, ymap, xmap, a, p->nctas, ncomp_sweep, smem, s);
 }
 
 int wide4_common(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
@@ -332,8 +759,8 @@ int wide4_common(tm_march_plan *p, const tm_layout *layout, const double *uold, 
     if (d_nbr && (!box_extents || box_extents[0] < 2 * kR || box_extents[1] < 2 * kR || box_extents[2] < 2 * kR))
         return fail(TM_ERR_INVALID, std::string(who) + ": fused halos need uniform boxes of at least 8^3 cells");
     if (p->ncols == 0) return TM_OK;
-    if (p->max_nx > 128 || p->max_ny > 16)
-        return fail(TM_ERR_INVALID, std::string(who) + ": columns must be <= 128 wide and <= 16 rows");
+    if (p->max_nx > 128 || p->max_ny > 32)
+        return fail(TM_ERR_INVALID, std::string(who) + ": columns must be <= 128 wide and <= 32 rows");
     W4Args a{};
     a.cols = p->d_cols;
     a.segs = p->d_segs;
@@ -363,9 +790,13 @@ int wide4_common(tm_march_plan *p, const tm_layout *layout, const double *uold, 
     if (smem > 220 * 1024)
         return fail(TM_ERR_INVALID, std::string(who) + ": column plane too large for shared memory");
     CUtensorMap map;
+    cudaStream_t s = as_stream(stream);
+    if (!d_nbr && w2_eligible(p)) return w2_common<false>(p, L, uold, a, ncomp_sweep, nullptr, s);
+    if (p->max_ny > 16)
+        return fail(TM_ERR_INVALID, std::string(who) + ": columns of more than 16 rows need widths <= 64 and row "
+                                                       "counts that are multiples of 4");
     rc = encode_plane_map(&map, L, uold, a.box_x, a.box_y);
     if (rc) return rc;
-    cudaStream_t s = as_stream(stream);
     return d_nbr ? wide4_dispatch<true>(map, a, p, ncomp_sweep, smem, s)
                  : wide4_dispatch<false>(map, a, p, ncomp_sweep, smem, s);
 }
@@ -379,6 +810,44 @@ int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold
                    double dtD, void *stream) {
     return wide4_common(p, layout, uold, unew, ncomp_sweep, coeffs5, dxi2_0, dxi2_1, dxi2_2, dtD, nullptr, nullptr,
                         stream, "tm_wide4_march");
+}
+
+int tm_wide4_march_nbr(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                       double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream) {
+    using namespace tmk;
+    if (!p) return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: null plan");
+    int rc = check_layout(layout, "tm_wide4_march_nbr");
+    if (rc) return rc;
+    const tm_layout &L = *layout;
+    if (L.nghost < kR || !uold || !unew || uold == unew || !coeffs5 || !d_nbr || !box_extents)
+        return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: needs nghost >= 4, distinct old/new fields, 5 coefficients, "
+                                    "the neighbour table and the box extents");
+    if (ncomp_sweep < 1 || ncomp_sweep > L.ncomp) return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: bad ncomp");
+    if (strides_of(L).comp >= ((int64_t)1 << 32))
+        return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: one component of a slot must hold < 2^32 doubles");
+    if (p->ncols == 0) return TM_OK;
+    const int nxv = box_extents[0], nyv = box_extents[1], nzv = box_extents[2];
+    // full-width columns of one shape, rows in groups of 4, halo boxes landing 128-B aligned
+    if (!(w2_eligible(p) && p->uniform_nx && p->uniform_ny && p->x0_common == L.xoff && p->max_nx == nxv &&
+          nxv % 4 == 0 && nyv % p->max_ny == 0 && nyv >= kR && nzv >= kR && L.ny - 2 * L.nghost == nyv &&
+          L.nz - 2 * L.nghost == nzv))
+        return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: needs uniform boxes (width a multiple of 4, <= 64, each "
+                                    "extent >= 4) cut into full-width columns of one height (a multiple of 4, <= 32)");
+    W4Args a{};
+    a.out = unew;
+    const double *c = coeffs5;
+    a.c0 = c[0];
+    a.c1 = c[1];
+    a.c2 = c[2];
+    a.c3 = c[3];
+    a.c4 = c[4];
+    a.d0 = dxi2_0;
+    a.d1 = dxi2_1;
+    a.d2 = dxi2_2;
+    a.dtD = dtD;
+    a.nbr = d_nbr;
+    return w2_common<true>(p, L, uold, a, ncomp_sweep, box_extents, as_stream(stream));
 }
 
 int tm_wide4_march_fused(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,

@@ -13,9 +13,12 @@ callers fill 4 ghost layers first, exactly as with the reference.
 
 ``Wide4Runner`` is the reference's step loop (fill_boundary; wide4_step)
 on the device: with uniform boxes of at least 8^3 its steps are ONE launch
-each (``tm_wide4_march_fused``: the epilogue writes the 4-deep face ghosts of
-the next step, so the loop needs no FillBoundary), replayed from a CUDA graph
-of step pairs; one regular FillBoundary closes each ``advance``.
+each, replayed from a CUDA graph of step pairs, and one regular FillBoundary
+closes each ``advance``.  Boxes up to 64 wide run Kernel W2
+(``tm_wide4_march_nbr``: 32-row columns, every 4-deep halo read from the face
+neighbour's valid cells, nothing written but valid cells); wider boxes run
+Kernel W with the face ghosts of the next step written by the epilogue
+(``tm_wide4_march_fused``).
 """
 
 from __future__ import annotations
@@ -90,15 +93,31 @@ def wide4_stable_dt(diffusivity: float, dx, safety: float = 0.9) -> float:
     return safety * 2.0 / lam
 
 
+W2_ROWS = 32  # Kernel W2 column height cap (8 warps x 4 rows)
+
+
+def _w2_rows(mf: MultiFab) -> int | None:
+    """Column height cap under which every box of ``mf`` cuts into Kernel W2
+    columns (width <= 64, even; row counts multiples of 4), else None."""
+    from .march import _even_chunks
+
+    exts = {mf.units[u].valid.extents for u in mf.local_units}
+    for nx, ny, _ in exts:
+        if nx > 64 or nx % 2 or ny % 2 or any(sz % 4 for _, sz in _even_chunks(ny, W2_ROWS)):
+            return None
+    return W2_ROWS if exts else None
+
+
 def wide4_plan(mf: MultiFab, max_rows: int | None = None, nctas: int | None = None) -> "_native.MarchPlan":
-    """Columns (full box width, <= 16 rows (8 when wider than 64), full z)
-    split into equal plane shares over one persistent CTA per SM."""
+    """Columns (full box width, full z) split into equal plane shares over one
+    persistent CTA per SM: up to 32 rows when every box fits Kernel W2, else
+    <= 16 rows (8 when wider than 64) for Kernel W."""
     from .march import march_columns, sm_count
 
     widest = max((mf.units[u].valid.extents[0] for u in mf.local_units), default=1)
     if widest > 128:
         raise ValueError("wide4 kernel supports boxes up to 128 cells wide in x")
-    rows = max_rows or (16 if widest <= 64 else 8)
+    rows = max_rows or _w2_rows(mf) or (16 if widest <= 64 else 8)
     key = ("wide4", rows, nctas, mf.layout, tuple(mf.local_units))
     plan = mf._plans.get(key)
     if plan is None:
@@ -147,12 +166,15 @@ def wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: 
 class Wide4Runner:
     """Owns an old/new pair and advances the wide4 diffusion ``n`` steps at a
     time; bit-identical to ``steps x (fill_boundary; wide4_step)``.  Fused
-    (default when eligible): one launch per step, face ghosts written by the
-    previous step's epilogue; unfused: FillBoundary + Kernel W per step."""
+    (default when eligible): one launch per step -- with ``nbr_halos`` (default
+    when the boxes allow Kernel W2) every halo is read from the face
+    neighbours' valid cells and no ghost is written; otherwise the previous
+    step's epilogue writes the face ghosts (Kernel W, scatter).  Unfused:
+    FillBoundary + Kernel W/W2 per step."""
 
     def __init__(self, mf: MultiFab, geom: Geometry, diffusivity: float, dt: float,
                  coeffs: StencilCoeffs8 | None = None, fused: bool | None = None,
-                 use_graph: bool | None = None):
+                 use_graph: bool | None = None, nbr_halos: bool | None = None):
         import torch
 
         from .march import face_neighbors, fusable
@@ -171,9 +193,21 @@ class Wide4Runner:
             raise ValueError("fused wide4 needs one rank and uniform boxes of at least 8^3 covering the domain")
         self.fused = can_fuse if fused is None else fused
         self.use_graph = (world == 1) if use_graph is None else (use_graph and world == 1)
+        self.nbr_halos = False
         if self.fused:
             self.nbr = torch.as_tensor(face_neighbors(mf, geom).reshape(-1), dtype=torch.int32, device=mf.device)
             self.box = (ctypes.c_int32 * 3)(*next(iter(ext)))
+            from .march import _even_chunks
+
+            nx, ny, _ = next(iter(ext))
+            # Kernel W2 with neighbour-sourced halos (no ghost writes at all): widths a multiple
+            # of 4, every box cut into columns of one height
+            can_nbr = (_w2_rows(mf) is not None and nx % 4 == 0
+                       and len({sz for _, sz in _even_chunks(ny, W2_ROWS)}) == 1)
+            if nbr_halos and not can_nbr:
+                raise ValueError("neighbour-sourced wide4 halos need box widths that are multiples of 4 (<= 64) "
+                                 "and box heights that cut into equal 4-row-multiple columns")
+            self.nbr_halos = can_nbr if nbr_halos is None else nbr_halos
         self._graph = None
         self._primed = False
         self.steps_done = 0
@@ -199,8 +233,15 @@ class Wide4Runner:
             return
         c = self.coeffs
         dxi2 = tuple(1.0 / d ** 2 for d in self.geom.dx)
-        plan = wide4_plan(old)
         cbuf = (ctypes.c_double * 5)(c.c0, c.c1, c.c2, c.c3, c.c4)
+        if self.nbr_halos:
+            plan = wide4_plan(old)
+            _native.check(_native.load().tm_wide4_march_nbr(
+                plan.handle, old.layout.to_c(), old.ptr, new.wptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
+                dxi2[0], dxi2[1], dxi2[2], self.diffusivity * self.dt, self.nbr.data_ptr(), self.box,
+                old.stream()), "tm_wide4_march_nbr")
+            return
+        plan = wide4_plan(old, 16 if old.units[old.local_units[0]].valid.extents[0] <= 64 else 8)
         _native.check(_native.load().tm_wide4_march_fused(
             plan.handle, old.layout.to_c(), old.ptr, new.wgptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
             dxi2[0], dxi2[1], dxi2[2], self.diffusivity * self.dt, self.nbr.data_ptr(), self.box, old.stream()),

@@ -184,16 +184,20 @@ def test_wide4_needs_four_ghosts(tm):
         tm.wide4_step(mf2.clone_empty(), mf2, geom, 1.0, 1e-5, None)
 
 
-@pytest.mark.parametrize("n,mgs,steps,graph", [
-    (64, 32, 5, True),     # 2^3 boxes of 32^3: 2 cells per lane (adjacent pair), odd step count
-    (40, 40, 4, False),    # one 40^3 box: every face its own periodic image
-    (48, 16, 3, True),     # 3^3 boxes of 16^3
-    (24, 8, 6, True),      # 8^3 boxes: the 4-deep faces of a box cover it completely
-    (96, 96, 2, False),    # 96 wide: 3 cells per lane... routed to 4 per lane, 8-row columns
+@pytest.mark.parametrize("n,mgs,steps,graph,nbr", [
+    (64, 32, 5, True, None),     # 2^3 boxes of 32^3: Kernel W2, one 32-row column per box, odd step count
+    (64, 32, 3, True, False),    # same boxes on Kernel W's scatter epilogue (16-row columns)
+    (40, 40, 4, False, None),    # one 40^3 box: every face its own periodic image; W2 with 20-row columns
+    (40, 40, 2, False, False),
+    (48, 16, 3, True, None),     # 3^3 boxes of 16^3
+    (24, 8, 6, True, None),      # 8^3 boxes: the 4-deep faces of a box cover it completely
+    (24, 8, 3, True, False),
+    (96, 96, 2, False, None),    # 96 wide: Kernel W (4 cells per lane, 8-row columns), scatter epilogue
 ])
-def test_fused_wide4_runner_matches_oracle(tm, n, mgs, steps, graph):
-    """One launch per step (FillBoundary fused into the epilogue) against the
-    whole-domain oracle and against the reference-structured unfused loop."""
+def test_fused_wide4_runner_matches_oracle(tm, n, mgs, steps, graph, nbr):
+    """One launch per step (neighbour-sourced halos, or FillBoundary fused into
+    the epilogue) against the whole-domain oracle and against the
+    reference-structured unfused loop."""
     w = dataclasses.replace(tm.CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
     glob = tm.make_init(w)
     geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
@@ -204,13 +208,45 @@ def test_fused_wide4_runner_matches_oracle(tm, n, mgs, steps, graph):
     for fused in (True, False):
         mf = tm.MultiFab(ba, 1, 4)
         mf.from_global(glob)
-        r = tm.Wide4Runner(mf, geom, 1.0, dt, coeffs, fused=fused, use_graph=graph)
+        r = tm.Wide4Runner(mf, geom, 1.0, dt, coeffs, fused=fused, use_graph=graph,
+                           nbr_halos=nbr if fused else None)
         assert r.fused == fused
-        outs.append(r.advance(steps).to_global().cpu().numpy()[0])
+        if fused:
+            assert r.nbr_halos == (mgs <= 64 if nbr is None else nbr)
+        res = r.advance(steps)
+        outs.append(res.to_global().cpu().numpy()[0])
+        if fused:  # the closing FillBoundary leaves the ghosts a fresh fill gives
+            ref = tm.MultiFab(ba, 1, 4)
+            ref.from_global(res.to_global())
+            tm.fill_boundary(ref, geom)
+            for u in res.local_units:  # whole grown boxes, ghosts included (not the row padding)
+                fa, fb = res.fab(u), ref.fab(u)
+                assert np.array_equal(fa.view(fa.abox, 0, 1).cpu().numpy(), fb.view(fb.abox, 0, 1).cpu().numpy())
         r.close()
     want = orc.wide4_periodic(glob[0], steps, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
     assert np.array_equal(outs[0], want)
     assert np.array_equal(outs[1], want)
+
+
+def test_wide4_production_shape(tm):
+    """The C2-shaped wide4 problem the bench times (256^3, 64 boxes of 64^3,
+    4 ghosts): Kernel W2 with neighbour-sourced halos (fused runner, graph
+    pairs), Kernel W2 on ghosts (reference loop) and the oracle, every cell."""
+    w = dataclasses.replace(tm.CONFIGS["C2"].scaled(256, 64, 3), nghost=4)
+    glob = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    dt = tm.wide4_stable_dt(1.0, (w.dx,) * 3)
+    coeffs = tm.derive_coeffs8()
+    want = orc.wide4_periodic(glob[0], 3, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
+    mf = tm.MultiFab(ba, 1, 4)
+    mf.from_global(glob)
+    r = tm.Wide4Runner(mf, geom, 1.0, dt, coeffs)
+    assert r.fused and r.nbr_halos
+    assert np.array_equal(r.advance(3).to_global().cpu().numpy()[0], want)
+    r.close()
+    fin, _ = run_device(tm, w, glob, coeffs, dt, 3)
+    assert np.array_equal(fin.to_global().cpu().numpy()[0], want)
 
 
 def test_fused_wide4_eligibility(tm):
