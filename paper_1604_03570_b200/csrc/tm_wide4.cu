@@ -313,10 +313,11 @@ int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int nco
 //
 // Work: 8 consumer warps; warp w owns rows 4w .. 4w+3 of the column, lane l the
 // cell pair (2l, 2l+1) of each row.  The z window (planes k-4 .. k+4 of the
-// warp's 8 cells) lives in registers and shifts by one plane per step.  A plane's stage stays resident
-// from landing until it is the centre plane (its x/y neighbours), then is
-// released; window-only planes (the 4 below / above a segment) are released on
-// landing.
+// warp's 8 cells, 144 registers) lives in registers and rotates by renaming (the
+// plane loop is unrolled 9x).  A plane's stage stays resident from landing until
+// it is the centre plane (its x/y neighbours), then is released; window-only
+// planes (the 4 below / above a segment) are released on landing.  A producer
+// warpgroup streams the planes (see wide4_col_kernel for the register split).
 //
 // Stage layout (doubles), bw = stage row width:
 //   GHOST (tm_wide4_march, ghosts filled by FillBoundary): one TMA box
@@ -326,11 +327,8 @@ int launch_wide4_one(const CUtensorMap &map, const W4Args &a, int nctas, int nco
 //          region 128-B aligned (TMA destination); halo rows/columns/planes come
 //          from the face neighbour's valid cells (own ghosts where there is none).
 // ---------------------------------------------------------------------------
-#ifndef TM_W2_NW
-#define TM_W2_NW 8
-#endif
-constexpr int kW2Warps = TM_W2_NW;     // consumer warps
-constexpr int kW2Rows = 32 / TM_W2_NW;  // rows per consumer warp
+constexpr int kW2Warps = 8;  // consumer warps (two warpgroups; 16 x 2 rows measured slower: 106 vs 93 us)
+constexpr int kW2Rows = 4;   // rows per consumer warp
 
 struct W2Args {
     const tm_block *cols;
@@ -446,6 +444,10 @@ __device__ __forceinline__ void w2_issue(const W2Args &A, const CUtensorMap *cma
 // 8 consumer warps (setmaxnreg.inc to 232).  An earlier producer-less variant (the warp
 // releasing a stage last issued its refill) put the issue latency on the slowest warp's
 // critical path: 95 vs this kernel's time on the fused C2-shaped step (profiles/r02).
+template <int V>
+struct IC {
+    static constexpr int value = V;
+};
 constexpr int kW2ProdRegs = 40, kW2ConsRegs = 232;
 
 template <bool NBR>
@@ -563,8 +565,8 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
             if (wact) load_rows(saddr(g + q), w[q]);
             if (q < kR || q >= nk + kR) release(g + q);  // never a centre plane
         }
-        auto body = [&](int kk) {
-            constexpr int ROT = 0;  // window slot m holds plane k-4+m (shifted after each plane)
+        auto body = [&](auto rotc, int kk) {
+            constexpr int ROT = decltype(rotc)::value;  // kk % 9: window slot of plane q is q % 9
             constexpr int CEN = (ROT + kR) % (2 * kR + 1);
             const uint32_t qn = g + (uint32_t)kk + 2 * kR;  // leading edge: plane k+4
             wait_plane(qn);
@@ -627,18 +629,32 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
             }
             release(qc);
             koff += pstep;
-#pragma unroll
-            for (int m = 0; m < 2 * kR; ++m)
-#pragma unroll
-                for (int i = 0; i < kW2Rows; ++i) {
-                    w[m][i][0] = w[m + 1][i][0];
-                    w[m][i][1] = w[m + 1][i][1];
-                }
         };
-        // (Renaming the window slots instead of shifting them needs the plane loop unrolled
-        // nine times; that code no longer fits the instruction cache: ncu r02, 'no
-        // instructions' the top stall.)
-        for (int kk = 0; kk < nk; ++kk) body(kk);
+        // nine bodies per trip: the window slots rotate by renaming, no register moves (a
+        // shifted window costs 128 moves per plane: 77.7 vs 70.4 us per fused C2-shaped step)
+        {
+            int kk = 0;
+            for (;;) {
+                if (kk >= nk) break;
+                body(IC<0>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<1>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<2>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<3>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<4>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<5>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<6>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<7>{}, kk++);
+                if (kk >= nk) break;
+                body(IC<8>{}, kk++);
+            }
+        }
         g += nk + 2 * kR;
     }
 }
