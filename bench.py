@@ -658,6 +658,52 @@ def config_records(args, peak):
         except Exception as e:  # noqa: BLE001 -- reported, the headline line still prints
             out[name] = {"error": f"{type(e).__name__}: {e}"[:300]}
         torch.cuda.empty_cache()
+    # the 9-point 8th-order stencil ("wide4") on the C2 shape with the
+    # 4 ghost layers it needs -- the fused runner (Kernel W2, neighbour-sourced halos, one
+    # launch per step) and the reference loop (fill_boundary + wide4_step per step)
+    try:
+        import dataclasses
+
+        w = dataclasses.replace(tm.CONFIGS["C2"], nghost=4)
+        geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+        ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+        mf = tm.MultiFab(ba, 1, 4, zero=False)
+        mf.data.uniform_()
+        dt = tm.wide4_stable_dt(1.0, geom.dx)
+        r = tm.Wide4Runner(mf, geom, 1.0, dt)
+        k = 20
+        r.advance(k)
+        ms = timed(lambda n: r.advance(n, finalize=False), k)
+        cells = w.cells
+        old, new = r.a, r.b
+        plan = tm.build_fill_plan(old, geom)
+
+        def refloop(n):
+            a_, b_ = old, new
+            for _ in range(n):
+                tm.fill_boundary(a_, geom, plan)
+                tm.wide4_step(b_, a_, geom, 1.0, dt)
+                a_, b_ = b_, a_
+
+        refloop(2)
+        ms_ref = timed(refloop, k)
+        out["wide4_C2shape"] = {
+            "value": cells / (ms * 1e-3), "ms_per_step": ms, "steps": k,
+            "roofline_frac": 16 * cells / (ms * 1e-3) / 1e9 / peak, "bytes_per_update": 16,
+            "step_impl": ("fused: one Kernel W2 launch per step, every 4-deep halo read from the face "
+                          "neighbours' valid cells" if r.fused and r.nbr_halos else
+                          "fused" if r.fused else "unfused"),
+            "reference_loop": {"ms_per_step": ms_ref, "value": cells / (ms_ref * 1e-3),
+                               "how": "fill_boundary (4 ghost layers) + wide4_step (Kernel W2 on ghosts), eager"},
+            "workload": f"wide4 (9-point 8th-order Laplacian, SURVEY §8f row 1): periodic {w.n}^3, "
+                        f"max_grid_size {w.max_grid_size} ({len(ba)} boxes), nghost 4, ncomp 1",
+            "unit": UNIT,
+        }
+        r.close()
+        del r, mf
+    except Exception as e:  # noqa: BLE001
+        out["wide4_C2shape"] = {"error": f"{type(e).__name__}: {e}"[:300]}
+    torch.cuda.empty_cache()
     return out
 
 
