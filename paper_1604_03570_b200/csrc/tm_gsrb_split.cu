@@ -29,7 +29,7 @@ namespace {
 
 using tmk::Segment;
 
-constexpr int kSStages = 4;
+constexpr int kSStages = 8;  // 4: 51.1 us per C4 pass, 8: 50.5 (16-row columns) / 48.9 (32 rows)
 
 // Entry e of a colour row sits at index e + kE0 of a row of wp = nx/2 + 8 doubles
 // (320 B for 64-wide boxes): every row's valid entries start on a 32-B sector
@@ -60,55 +60,109 @@ __host__ __device__ inline ColourLayout colour_layout(int nslots, int nx, int ny
     return C;
 }
 
-// phi (valid + one ghost layer) -> both colour arrays; rhs -> both colour rhs arrays
+// phi (valid + one ghost layer) -> both colour arrays; rhs -> both colour rhs arrays.
+// One warp per row (slot, z, y): lane l loads the cell pair x = 2l, 2l+1 with one 16-B load
+// (rows start 128-B aligned), which holds entry l of both colours -- colour c's entry sits at
+// offset o_c = (c + parity + y + z) & 1 of the pair -- and stores them with two coalesced
+// 8-B stores.  The two x-ghost entries (x = -1 and x = nx) come from lanes 0 and 31.
+// (r01's thread-per-entry gather: 242 us per C4 solve for split, 114 for merge + fill.)
 __global__ void split_kernel(tm_layout L, const double *__restrict__ phi, ColourLayout C, const int32_t *parity,
                              double *__restrict__ c0, double *__restrict__ c1, tm_layout R,
                              const double *__restrict__ rhs, double *__restrict__ r0, double *__restrict__ r1) {
+    // kB rows per warp and trip, their loads issued together (one row in flight per warp left
+    // the kernel latency-bound: 187 us per C4 split); 32-bit row indices (host-checked)
+    constexpr int kB = 4;
     const int nh = C.nx / 2;
-    const int64_t rows = (int64_t)C.nslots * (C.nz + 2) * (C.ny + 2);
+    const int lane = threadIdx.x & 31;
+    const int rows = C.nslots * (C.nz + 2) * (C.ny + 2);
+    const int wstride = gridDim.x * (blockDim.x >> 5) * kB;
     const tmk::Strides s = tmk::strides_of(L);
     const tmk::Strides rs = tmk::strides_of(R);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.y + threadIdx.y; t < rows; t += (int64_t)gridDim.x * blockDim.y) {
-        const int yy = (int)(t % (C.ny + 2)), zz = (int)((t / (C.ny + 2)) % (C.nz + 2));
-        const int slot = (int)(t / ((int64_t)(C.ny + 2) * (C.nz + 2)));
-        const int y = yy - 1, z = zz - 1;
-        const double *prow = phi + slot * s.slot + (int64_t)(z + L.nghost) * s.plane + (int64_t)(y + L.nghost) * s.row +
-                             L.xoff;
-        const bool valid_row = y >= 0 && y < C.ny && z >= 0 && z < C.nz;
-        for (int i = (int)threadIdx.x - 1; i <= nh; i += blockDim.x) {
+    for (int t0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kB; t0 < rows; t0 += wstride) {
+        for (int e = lane; e < nh; e += 32) {
+            double2 v[kB], rv[kB];
+            int o0[kB];
+            bool vr[kB];
+            int64_t dro[kB], rro[kB];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int o = (c + parity[slot] + y + z) & 1;
-                const int x = 2 * i + o;
-                double *dst = (c ? c1 : c0) + slot * C.slot + (int64_t)zz * C.plane + (int64_t)yy * C.row + (i + kE0);
-                if (x >= -1 && x <= C.nx) *dst = prow[x];
-                if (rhs && valid_row && i >= 0 && i < nh) {
-                    const double *rrow = rhs + slot * rs.slot + (int64_t)(z + R.nghost) * rs.plane +
-                                         (int64_t)(y + R.nghost) * rs.row + R.xoff;
-                    (c ? r1 : r0)[slot * C.rslot + (int64_t)z * C.rplane + (int64_t)y * C.rrow + i] = rrow[x];
+            for (int b = 0; b < kB; ++b) {
+                const int t = min(t0 + b, rows - 1);
+                const int yy = t % (C.ny + 2), zs = t / (C.ny + 2);
+                const int zz = zs % (C.nz + 2), slot = zs / (C.nz + 2);
+                const int y = yy - 1, z = zz - 1;
+                o0[b] = (parity[slot] + y + z) & 1;  // x offset of colour 0's entries in this row
+                dro[b] = slot * C.slot + (int64_t)zz * C.plane + (int64_t)yy * C.row + kE0;
+                v[b] = *reinterpret_cast<const double2 *>(phi + slot * s.slot + (int64_t)(z + L.nghost) * s.plane +
+                                                          (int64_t)(y + L.nghost) * s.row + L.xoff + 2 * e);
+                vr[b] = rhs && y >= 0 && y < C.ny && z >= 0 && z < C.nz && t0 + b < rows;
+                rro[b] = slot * C.rslot + (int64_t)z * C.rplane + (int64_t)y * C.rrow;
+                if (vr[b])
+                    rv[b] = *reinterpret_cast<const double2 *>(rhs + slot * rs.slot + (int64_t)(z + R.nghost) * rs.plane +
+                                                               (int64_t)(y + R.nghost) * rs.row + R.xoff + 2 * e);
+            }
+#pragma unroll
+            for (int b = 0; b < kB; ++b) {
+                if (t0 + b >= rows) continue;
+                c0[dro[b] + e] = o0[b] ? v[b].y : v[b].x;
+                c1[dro[b] + e] = o0[b] ? v[b].x : v[b].y;
+                if (vr[b]) {
+                    r0[rro[b] + e] = o0[b] ? rv[b].y : rv[b].x;
+                    r1[rro[b] + e] = o0[b] ? rv[b].x : rv[b].y;
                 }
+            }
+        }
+        // ghost entries: entry -1 of the colour at offset 1 is x = -1, entry nh of the colour at
+        // offset 0 is x = nx
+        if (lane < 2 * kB) {
+            const int t = t0 + (lane >> 1);
+            if (t < rows) {
+                const int yy = t % (C.ny + 2), zs = t / (C.ny + 2);
+                const int zz = zs % (C.nz + 2), slot = zs / (C.nz + 2);
+                const int y = yy - 1, z = zz - 1;
+                const int o0 = (parity[slot] + y + z) & 1;
+                const double *prow = phi + slot * s.slot + (int64_t)(z + L.nghost) * s.plane +
+                                     (int64_t)(y + L.nghost) * s.row + L.xoff;
+                const int64_t ro = slot * C.slot + (int64_t)zz * C.plane + (int64_t)yy * C.row + kE0;
+                if ((lane & 1) == 0)
+                    (o0 ? c0 : c1)[ro - 1] = prow[-1];
+                else
+                    (o0 ? c1 : c0)[ro + nh] = prow[C.nx];
             }
         }
     }
 }
 
-// both colour arrays -> phi valid cells
+// both colour arrays -> phi valid cells (one warp per kB rows, one 16-B store per cell pair)
 __global__ void merge_kernel(tm_layout L, double *__restrict__ phi, ColourLayout C, const int32_t *parity,
                              const double *__restrict__ c0, const double *__restrict__ c1) {
+    constexpr int kB = 4;
     const int nh = C.nx / 2;
-    const int64_t rows = (int64_t)C.nslots * C.nz * C.ny;
+    const int lane = threadIdx.x & 31;
+    const int rows = C.nslots * C.nz * C.ny;
+    const int wstride = gridDim.x * (blockDim.x >> 5) * kB;
     const tmk::Strides s = tmk::strides_of(L);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.y + threadIdx.y; t < rows; t += (int64_t)gridDim.x * blockDim.y) {
-        const int y = (int)(t % C.ny), z = (int)((t / C.ny) % C.nz);
-        const int slot = (int)(t / ((int64_t)C.ny * C.nz));
-        double *prow = phi + slot * s.slot + (int64_t)(z + L.nghost) * s.plane + (int64_t)(y + L.nghost) * s.row + L.xoff;
-        for (int i = threadIdx.x; i < nh; i += blockDim.x) {
+    for (int t0 = (blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * kB; t0 < rows; t0 += wstride) {
+        for (int e = lane; e < nh; e += 32) {
+            double a0[kB], a1[kB];
+            double *dst[kB];
+            int o0[kB];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                const int o = (c + parity[slot] + y + z) & 1;
-                prow[2 * i + o] =
-                    (c ? c1 : c0)[slot * C.slot + (int64_t)(z + 1) * C.plane + (int64_t)(y + 1) * C.row + (i + kE0)];
+            for (int b = 0; b < kB; ++b) {
+                const int t = min(t0 + b, rows - 1);
+                const int y = t % C.ny, zs = t / C.ny;
+                const int z = zs % C.nz, slot = zs / C.nz;
+                o0[b] = (parity[slot] + y + z) & 1;
+                const int64_t ro = slot * C.slot + (int64_t)(z + 1) * C.plane + (int64_t)(y + 1) * C.row + kE0 + e;
+                a0[b] = c0[ro];
+                a1[b] = c1[ro];
+                dst[b] = phi + slot * s.slot + (int64_t)(z + L.nghost) * s.plane + (int64_t)(y + L.nghost) * s.row +
+                         L.xoff + 2 * e;
             }
+#pragma unroll
+            for (int b = 0; b < kB; ++b)
+                if (t0 + b < rows)
+                    *reinterpret_cast<double2 *>(dst[b]) =
+                        o0[b] ? make_double2(a1[b], a0[b]) : make_double2(a0[b], a1[b]);
         }
     }
 }
@@ -189,43 +243,53 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
     };
     const double h2 = a.h2;
     const uint32_t ystep = (uint32_t)wp * 8u;
+    // Hot-loop bookkeeping: per-segment row pointers and scatter targets, one running 32-bit
+    // plane offset and a parity bit that flips per plane (r01 recomputed 64-bit addresses and
+    // every scatter condition per cell).  Neither this, an 8-deep ring nor an early stage
+    // release moves the pass much (50.8 / 50.5 / 52.1 us, r02): it streams at ~4.7 TB/s.
+    const uint32_t cplane = (uint32_t)C.plane;  // host-checked < 2^31
     uint32_t g = 0;
     for (int s = s_begin; s < s_end; ++s) {
         const Segment sg = a.segs[s];
         const tm_block c = a.cols[sg.col];
         const int nk = sg.k1 - sg.k0;
         const int yv0 = c.y0 - 1, zv0 = c.z0 - 1 + sg.k0;  // valid y of row 0, valid z of the first plane
-        // neighbour slot deltas in registers (the scatter stores could alias a global table)
-        int64_t dn[6];
-        bool hn[6];
-#pragma unroll
-        for (int f = 0; f < 6; ++f) {
-            const int32_t t = a.nbr[6 * c.slot + f];
-            hn[f] = t >= 0;
-            dn[f] = (int64_t)(t - c.slot) * C.slot;
-        }
-        dn[0] += nh;                        // x = 0 -> -x neighbour's entry nh
-        dn[1] -= nh;                        // x = nx-1 -> +x neighbour's entry -1
-        dn[2] += (int64_t)C.ny * C.row;     // row 0 -> -y neighbour's row ny
-        dn[3] -= (int64_t)C.ny * C.row;     // row ny-1 -> +y neighbour's row -1
-        dn[4] += (int64_t)C.nz * C.plane;   // plane 0 -> -z neighbour's plane nz
-        dn[5] -= (int64_t)C.nz * C.plane;   // plane nz-1 -> +z neighbour's plane -1
+        const int32_t *nbp = a.nbr + 6 * c.slot;
         const bool lane_on = lane * CPL < nh;
         const int ii = min(lane * CPL, nh - CPL);  // lane's first entry
-        int rr[RPW];
-        bool on[RPW];
         uint32_t so[RPW], ro[RPW];  // stage byte offsets: other colour at (row, entry ii), rhs
-        double *orow[RPW];
+        double *orow[RPW];          // colour-c cells of the row at the segment's first plane
+        double *ysc[RPW];           // the -y / +y neighbour's ghost row entry, or null
+        bool on[RPW];
+        int o0[RPW];                // entry -> x offset of the colour at plane k0 (flips per plane)
+        double *const sbase_out = a.out + (int64_t)c.slot * C.slot + (int64_t)(zv0 + 1) * C.plane + (ii + kE0);
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
             const int r = warp * RPW + i;
-            rr[i] = r;
             on[i] = lane_on && r < c.ny;
             const int rc = min(r, R - 1);
             so[i] = (uint32_t)((rc + 1) * wp + ii + 2) * 8u;
             ro[i] = (uint32_t)(a.rhs_off + rc * nh + ii) * 8u;
-            orow[i] = a.out + c.slot * C.slot + (int64_t)(yv0 + r + 1) * C.row + (ii + kE0);
+            orow[i] = sbase_out + (int64_t)(yv0 + r + 1) * C.row;
+            o0[i] = (a.color + c.parity + r + sg.k0) & 1;
+            const int yv = yv0 + r;
+            ysc[i] = nullptr;
+            if (on[i] && yv == 0 && nbp[2] >= 0)  // row 0 -> the -y neighbour's row ny
+                ysc[i] = orow[i] + (int64_t)(nbp[2] - c.slot) * C.slot + (int64_t)C.ny * C.row;
+            else if (on[i] && yv == C.ny - 1 && nbp[3] >= 0)  // row ny-1 -> the +y neighbour's row -1
+                ysc[i] = orow[i] + (int64_t)(nbp[3] - c.slot) * C.slot - (int64_t)C.ny * C.row;
         }
+        // x faces: entry 0 at offset 0 is x = 0 (-> the -x neighbour's entry nh); entry nh-1 at
+        // offset 1 is x = nx-1 (-> the +x neighbour's entry -1)
+        const bool xlo = lane_on && ii == 0 && nbp[0] >= 0;
+        const bool xhi = lane_on && ii + CPL == nh && nbp[1] >= 0;
+        const int64_t dxlo = (int64_t)(nbp[0] - c.slot) * C.slot + nh;
+        const int64_t dxhi = (int64_t)(nbp[1] - c.slot) * C.slot - nh;
+        // z faces: plane 0 -> the -z neighbour's plane nz, plane nz-1 -> the +z neighbour's plane -1
+        const int kzlo = (nbp[4] >= 0 && zv0 <= 0 && 0 < zv0 + nk) ? -zv0 : -1;
+        const int kzhi = (nbp[5] >= 0 && zv0 <= C.nz - 1 && C.nz - 1 < zv0 + nk) ? C.nz - 1 - zv0 : -1;
+        const int64_t dzlo = (int64_t)(nbp[4] - c.slot) * C.slot + (int64_t)C.nz * C.plane;
+        const int64_t dzhi = (int64_t)(nbp[5] - c.slot) * C.slot - (int64_t)C.nz * C.plane;
         // z march state per cell: the other colour's value below (carried)
         double ob[RPW][CPL];
         wait_plane(g);
@@ -238,19 +302,21 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
                 for (int j = 0; j < CPL; ++j) ob[i][j] = lds_f64(s0 + so[i] + 8u * j);
         }
         release(g);
+        uint32_t kofs = 0;  // kk * C.plane
         for (int kk = 0; kk < nk; ++kk) {
             const uint32_t gc = g + 1 + (uint32_t)kk;
             wait_plane(gc + 1);
             const uint32_t sc = saddr(gc), sn = saddr(gc + 1);
-            const int zv = zv0 + kk;
             double out[RPW][CPL];
+            int oo[RPW];
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
+                oo[i] = o0[i] ^ (kk & 1);
+                const uint32_t ox = 8u * (uint32_t)oo[i];
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) {
-                    const int o = (a.color + c.parity + rr[i] + sg.k0 + kk) & 1;
                     const uint32_t p = sc + so[i] + 8u * j;
-                    const double w = lds_f64(p - 8u + 8u * o), e = lds_f64(p + 8u * o);
+                    const double w = lds_f64(p - 8u + ox), e = lds_f64(p + ox);
                     const double sv = lds_f64(p - ystep), nv = lds_f64(p + ystep);
                     const double t = lds_f64(sn + so[i] + 8u * j);
                     const double rh = lds_f64(sc + ro[i] + 8u * j);
@@ -263,31 +329,26 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
 #pragma unroll
             for (int i = 0; i < RPW; ++i) {
                 if (!on[i]) continue;
-                double *d = orow[i] + (int64_t)(zv + 1) * C.plane;
+                double *d = orow[i] + kofs;
 #pragma unroll
                 for (int j = 0; j < CPL; ++j) d[j] = out[i][j];
-                // fused FillBoundary of this colour: face neighbours' ghost entries
-                const int yv = yv0 + rr[i];
-                const int o = (a.color + c.parity + rr[i] + sg.k0 + kk) & 1;
+                // fused FillBoundary of this colour: the face neighbours' ghost entries
+                if (ysc[i]) {
 #pragma unroll
-                for (int j = 0; j < CPL; ++j) {
-                    const int e_i = ii + j;
-                    if (o == 0 && e_i == 0 && hn[0]) d[j + dn[0]] = out[i][j];
-                    if (o == 1 && e_i == nh - 1 && hn[1]) d[j + dn[1]] = out[i][j];
+                    for (int j = 0; j < CPL; ++j) ysc[i][kofs + j] = out[i][j];
                 }
-                const bool sy = (yv == 0 && hn[2]) || (yv == C.ny - 1 && hn[3]);
-                if (sy) {
-                    const int64_t dy = yv == 0 ? dn[2] : dn[3];
+                if (kk == kzlo) {
 #pragma unroll
-                    for (int j = 0; j < CPL; ++j) d[j + dy] = out[i][j];
+                    for (int j = 0; j < CPL; ++j) d[dzlo + j] = out[i][j];
                 }
-                const bool sz = (zv == 0 && hn[4]) || (zv == C.nz - 1 && hn[5]);
-                if (sz) {
-                    const int64_t dz = zv == 0 ? dn[4] : dn[5];
+                if (kk == kzhi) {
 #pragma unroll
-                    for (int j = 0; j < CPL; ++j) d[j + dz] = out[i][j];
+                    for (int j = 0; j < CPL; ++j) d[dzhi + j] = out[i][j];
                 }
+                if (xlo && oo[i] == 0) d[dxlo] = out[i][0];
+                if (xhi && oo[i] == 1) d[dxhi + CPL - 1] = out[i][CPL - 1];
             }
+            kofs += cplane;
         }
         release(g + (uint32_t)nk + 1);
         g += (uint32_t)nk + 2;
@@ -348,8 +409,10 @@ int tm_gsrb_split(const tm_layout *phi_layout, const double *phi, int32_t nx, in
         (rhs && (!r0 || !r1)))
         return fail(TM_ERR_INVALID, "tm_gsrb_split: bad arguments (nx must be a multiple of 4, nghost >= 1)");
     const ColourLayout C = colour_layout(phi_layout->nslots, nx, ny, nz);
+    if ((int64_t)C.nslots * (nz + 2) * (ny + 2) >= ((int64_t)1 << 31))
+        return fail(TM_ERR_INVALID, "tm_gsrb_split: too many rows");
     const tm_layout R = rhs ? *rhs_layout : *phi_layout;
-    split_kernel<<<592, dim3(32, 8), 0, as_stream(stream)>>>(*phi_layout, phi, C, d_parity, c0, c1, R, rhs, r0, r1);
+    split_kernel<<<148 * 8, 256, 0, as_stream(stream)>>>(*phi_layout, phi, C, d_parity, c0, c1, R, rhs, r0, r1);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TM_OK : cuda_fail(e, "tm_gsrb_split launch");
 }
@@ -362,7 +425,8 @@ int tm_gsrb_merge(const tm_layout *phi_layout, double *phi, int32_t nx, int32_t 
     if (!phi || !c0 || !c1 || !d_parity || nx % 4 || nx < 4)
         return fail(TM_ERR_INVALID, "tm_gsrb_merge: bad arguments");
     const ColourLayout C = colour_layout(phi_layout->nslots, nx, ny, nz);
-    merge_kernel<<<592, dim3(32, 8), 0, as_stream(stream)>>>(*phi_layout, phi, C, d_parity, c0, c1);
+    if ((int64_t)C.nslots * nz * ny >= ((int64_t)1 << 31)) return fail(TM_ERR_INVALID, "tm_gsrb_merge: too many rows");
+    merge_kernel<<<148 * 8, 256, 0, as_stream(stream)>>>(*phi_layout, phi, C, d_parity, c0, c1);
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? TM_OK : cuda_fail(e, "tm_gsrb_merge launch");
 }
@@ -376,6 +440,8 @@ int tm_gsrb_split_pass(tm_march_plan *p, int32_t nslots, int32_t nx, int32_t ny,
         return fail(TM_ERR_INVALID, "tm_gsrb_split_pass: bad arguments");
     if (p->ncols == 0) return TM_OK;
     if (p->max_nx != nx || p->max_ny > 32) return fail(TM_ERR_INVALID, "tm_gsrb_split_pass: columns must span the box width, <= 32 rows");
+    if (colour_layout(nslots, nx, ny, nz).plane * (int64_t)(nz + 2) >= ((int64_t)1 << 31))
+        return fail(TM_ERR_INVALID, "tm_gsrb_split_pass: one slot of a colour array must hold < 2^31 doubles");
     SplitArgs a{};
     a.cols = p->d_cols;
     a.segs = p->d_segs;
@@ -389,6 +455,9 @@ int tm_gsrb_split_pass(tm_march_plan *p, int32_t nslots, int32_t nx, int32_t ny,
     a.rhs_off = (((a.C.nx / 2 + 4) * a.box_y + 15) / 16) * 16;
     a.stage_elems = a.rhs_off + ((nx / 2 * p->max_ny + 15) / 16) * 16;
     const size_t smem = (size_t)kSStages * a.stage_elems * sizeof(double) + 2 * kSStages * sizeof(uint64_t);
+    if (smem > 220 * 1024)
+        return fail(TM_ERR_INVALID, "tm_gsrb_split_pass: column plane too large for the shared-memory ring (use "
+                                    "fewer rows per column)");
     CUtensorMap omap, rmap;
     int rc = encode_colour_map(&omap, a.C, other, a.box_y);
     if (rc) return rc;
