@@ -36,6 +36,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static std::once_flag g_encode_once;
 
 int encode_plane_map(CUtensorMap *map, const tm_layout &L, const double *base, int box_x, int box_y) {
+    Strides s = strides_of(L);
+    return encode_plane_map_strided(map, base, L.pitch, L.ny, L.nz, L.nslots * L.ncomp, s.plane, s.comp, box_x, box_y);
+}
+
+int encode_plane_map_strided(CUtensorMap *map, const double *base, int64_t pitch, int64_t ny, int64_t nz, int64_t nw,
+                             int64_t plane_stride, int64_t w_stride, int box_x, int box_y) {
     std::call_once(g_encode_once, [] {
         void *fn = nullptr;
         cudaDriverEntryPointQueryResult q;
@@ -47,10 +53,8 @@ int encode_plane_map(CUtensorMap *map, const tm_layout &L, const double *base, i
     if (box_x < 2 || box_x > 256 || (box_x & 1) || box_y < 1 || box_y > 256)
         return fail(TM_ERR_INVALID, "TMA plane box out of range");
     if ((reinterpret_cast<uintptr_t>(base) & 15) != 0) return fail(TM_ERR_INVALID, "storage not 16-B aligned");
-    Strides s = strides_of(L);
-    cuuint64_t dims[4] = {(cuuint64_t)L.pitch, (cuuint64_t)L.ny, (cuuint64_t)L.nz,
-                          (cuuint64_t)(L.nslots * L.ncomp)};
-    cuuint64_t gstr[3] = {(cuuint64_t)(s.row * 8), (cuuint64_t)(s.plane * 8), (cuuint64_t)(s.comp * 8)};
+    cuuint64_t dims[4] = {(cuuint64_t)pitch, (cuuint64_t)ny, (cuuint64_t)nz, (cuuint64_t)nw};
+    cuuint64_t gstr[3] = {(cuuint64_t)(pitch * 8), (cuuint64_t)(plane_stride * 8), (cuuint64_t)(w_stride * 8)};
     cuuint32_t box[4] = {(cuuint32_t)box_x, (cuuint32_t)box_y, 1, 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double *>(base), dims, gstr, box,

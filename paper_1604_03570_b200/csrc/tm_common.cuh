@@ -37,6 +37,9 @@ int check_layout(const tm_layout *L, const char *who);
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda)
 int encode_plane_map(CUtensorMap *map, const tm_layout &L, const double *base, int box_x, int box_y);
+// the same with explicit element strides of a plane and of a (slot, component) block
+int encode_plane_map_strided(CUtensorMap *map, const double *base, int64_t pitch, int64_t ny, int64_t nz, int64_t nw,
+                             int64_t plane_stride, int64_t w_stride, int box_x, int box_y);
 
 // ---------------------------------------------------------------- device PTX
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
