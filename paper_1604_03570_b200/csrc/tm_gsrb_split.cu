@@ -207,7 +207,9 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 8 ? 2 : 1)
         }
         fence_mbar_init();
     }
+    grid_dep_launch();  // the next pass's CTAs may take SM slots as ours retire
     __syncthreads();
+    grid_dep_wait();  // previous pass complete: it wrote the colour we read (and read the one we write)
 
     if (warp == NWARP) {  // ---------------- producer warp ----------------
         if (lane == 0) {
@@ -367,8 +369,18 @@ int launch_split_one(const CUtensorMap &omap, const CUtensorMap &rmap, const Spl
         if (e != cudaSuccess) return tmk::cuda_fail(e, "cudaFuncSetAttribute(gsrb split)");
         configured = true;
     }
-    kern<<<nctas, (NWARP + 1) * 32, smem, s>>>(omap, rmap, a);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(nctas);
+    cfg.blockDim = dim3((NWARP + 1) * 32);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, omap, rmap, a);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return tmk::cuda_fail(e, "gsrb split launch");
     return TM_OK;
 }

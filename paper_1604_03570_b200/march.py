@@ -482,6 +482,9 @@ class FusedGSRB:
     Bit-identical to ``stencil.gsrb_sweep`` (red, FillBoundary, black,
     FillBoundary)."""
 
+    LONG = 8  # sweeps per replay of the long graph
+    _long = None
+
     def __init__(self, phi: MultiFab, rhs: MultiFab, geom: Geometry, max_rows: int | None = None,
                  nctas: int | None = None):
         import torch
@@ -538,6 +541,19 @@ class FusedGSRB:
                     self.sweep()
             cur.wait_stream(s)
             self._graph = g
+            # a second graph chaining LONG sweeps: every replay is a graph launch (~2 us)
+            gl = torch.cuda.CUDAGraph()
+            s.wait_stream(cur)
+            with torch.cuda.stream(s):
+                with torch.cuda.graph(gl, stream=s):
+                    for _ in range(self.LONG):
+                        self.sweep()
+            cur.wait_stream(s)
+            self._long = gl
+        if use_graph and getattr(self, "_long", None) is not None and self._graph is not None:
+            while sweeps - k >= self.LONG:
+                self._long.replay()
+                k += self.LONG
         for _ in range(k, sweeps):
             if use_graph and self._graph is not None:
                 self._graph.replay()
@@ -570,6 +586,9 @@ class SplitGSRB:
     launch reading only the other colour (and filling the face ghosts of its
     own), ``finalize`` merges back into phi and runs FillBoundary.
     Bit-identical to ``stencil.gsrb_sweep``."""
+
+    LONG = FusedGSRB.LONG
+    _long = None
 
     def __init__(self, phi: MultiFab, rhs: MultiFab, geom: Geometry, max_rows: int | None = None,
                  nctas: int | None = None):

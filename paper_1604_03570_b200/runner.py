@@ -43,6 +43,8 @@ from .stencil import HeatParams, heat_step, overlapped_step
 class HeatRunner:
     """Owns the old/new pair and advances it ``n`` steps at a time."""
 
+    LONG_PAIRS = 8  # captured pairs per replay of the long graph (one rank)
+
     def __init__(self, mf: MultiFab, geom: Geometry, params: HeatParams, schedule=None,
                  plan: FillPlan | None = None, use_graph: bool | None = None, zmerge: bool = False,
                  fused: bool | None = None, march_rows: int | None = None):
@@ -67,6 +69,7 @@ class HeatRunner:
         self.fused = can_fuse if fused is None else fused
         self.fh = march.FusedHalo(self.a, self.b, geom, march_rows, fill_plan=self.plan) if self.fused else None
         self._graph = None
+        self._long = None  # one-rank: LONG_PAIRS captured pairs per replay (see advance)
         self._graph_pairs = 2 if (not self.fused and world == 1) else 1
         self._primed = False
         self.steps_done = 0
@@ -100,6 +103,7 @@ class HeatRunner:
         if self._graph is not None:
             torch.cuda.synchronize()
             self._graph = None
+            self._long = None
 
     def _step(self, old: MultiFab, new: MultiFab) -> None:
         if self.fused:  # b -> a steps walk backwards: they start where a -> b ended (L2)
@@ -134,6 +138,18 @@ class HeatRunner:
         self._graph = g
         if self._check_graph:
             self._verify_capture()
+        elif self.LONG_PAIRS > 1:
+            # one rank: a second graph chaining LONG_PAIRS captured pairs; each replay of the
+            # pair graph costs a graph launch (~1.4 us per C2 step at 2 steps per replay)
+            gl = torch.cuda.CUDAGraph()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s), snapshots_in_capture():
+                with torch.cuda.graph(gl, stream=s):
+                    for _ in range(self.LONG_PAIRS * self._graph_pairs):
+                        self._step(self.a, self.b)
+                        self._step(self.b, self.a)
+            torch.cuda.current_stream().wait_stream(s)
+            self._long = gl
 
     def _verify_capture(self) -> None:
         """Multi-rank: replay the captured pair once and redo the same two
@@ -178,6 +194,11 @@ class HeatRunner:
                 self._capture()
                 self.steps_done += need
                 k += need
+            if self.steps_done % 2 == 0 and self._long is not None:
+                while n - k >= 2 * self._graph_pairs * self.LONG_PAIRS:
+                    self._long.replay()
+                    self.steps_done += 2 * self._graph_pairs * self.LONG_PAIRS
+                    k += 2 * self._graph_pairs * self.LONG_PAIRS
             if self.steps_done % 2 == 0 and self._graph is not None:
                 while n - k >= 2 * self._graph_pairs:
                     self._graph.replay()

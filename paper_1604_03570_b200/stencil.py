@@ -346,7 +346,7 @@ def gsrb_solve(phi: MultiFab, rhs: MultiFab, geom: Geometry, sweeps: int, schedu
             phi._plans[key] = fg
         elif fg.rhs is not rhs:  # same layout, new array: rebind (the captured graph holds rhs pointers)
             fg.rhs = rhs
-            fg._graph = None
+            fg._graph = fg._long = None
         fg.prime(plan)
         fg.run(sweeps)
         fg.finalize(plan)
