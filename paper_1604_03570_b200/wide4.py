@@ -172,6 +172,9 @@ class Wide4Runner:
     step's epilogue writes the face ghosts (Kernel W, scatter).  Unfused:
     FillBoundary + Kernel W/W2 per step."""
 
+    LONG_PAIRS = 8  # captured pairs per replay of the long graph
+    _long = None
+
     def __init__(self, mf: MultiFab, geom: Geometry, diffusivity: float, dt: float,
                  coeffs: StencilCoeffs8 | None = None, fused: bool | None = None,
                  use_graph: bool | None = None, nbr_halos: bool | None = None):
@@ -222,7 +225,7 @@ class Wide4Runner:
         self._primed = False
 
     def close(self) -> None:
-        self._graph = None
+        self._graph = self._long = None
 
     def _step(self, old: MultiFab, new: MultiFab) -> None:
         from .multifab import fill_boundary
@@ -261,6 +264,14 @@ class Wide4Runner:
             self._step(self.b, self.a)
         torch.cuda.current_stream().wait_stream(s)
         self._graph = g
+        gl = torch.cuda.CUDAGraph()  # LONG_PAIRS pairs per replay: one graph launch per 16 steps
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s), torch.cuda.graph(gl, stream=s):
+            for _ in range(self.LONG_PAIRS):
+                self._step(self.a, self.b)
+                self._step(self.b, self.a)
+        torch.cuda.current_stream().wait_stream(s)
+        self._long = gl
 
     def advance(self, n: int, finalize: bool = True) -> MultiFab:
         """Advance ``n`` steps; returns the MultiFab holding the state (all
@@ -276,6 +287,10 @@ class Wide4Runner:
                 self._capture()  # two real steps
                 self.steps_done += 2
                 k += 2
+            while n - k >= 2 * self.LONG_PAIRS:
+                self._long.replay()
+                self.steps_done += 2 * self.LONG_PAIRS
+                k += 2 * self.LONG_PAIRS
             while n - k >= 2:
                 self._graph.replay()
                 self.steps_done += 2
