@@ -381,6 +381,7 @@ class FusedHalo:
         # computed exactly once, by the same kernel, so results do not change.
         self.plan_b = self.plan_i = None
         self.comm = None
+        self.timeline = None  # a list: each multi-rank step appends its phase events
         if multi:
             cols = self.plan.columns
             # "boundary" slots: every slot whose cells travel to another rank (the source of
@@ -465,14 +466,34 @@ class FusedHalo:
             exchange()
             return
         main = torch.cuda.current_stream(new.device)
+        tl = self.timeline  # optional: CUDA events marking the phases (tools/overlap_timeline.py)
+        marks = None
+        if tl is not None:
+            marks = {k: torch.cuda.Event(enable_timing=True) for k in (
+                "start", "boundary_done", "interior_start", "interior_done", "exchange_start", "exchange_done")}
+            marks["start"].record(main)
         march(self.plan_b)
-        # the exchange reads the boundary boxes' valid cells and writes only ghost cells of remote
-        # faces (and their x halos); the interior columns write other cells, so the two run
-        # concurrently; the next step waits for both
-        self.comm.wait_stream(main)
-        with torch.cuda.stream(self.comm):
-            exchange()
+        boundary_done = torch.cuda.Event(enable_timing=tl is not None)
+        boundary_done.record(main)
+        # the interior columns are enqueued BEFORE the exchange: a host-blocking exchange (gloo)
+        # then runs while they march, and an NCCL one on the side stream concurrently with them.
+        # The exchange reads only the boundary planes' valid cells and writes only ghost cells of
+        # remote faces (and their x halos); the interior march writes other cells
+        if tl is not None:
+            marks["interior_start"].record(main)
         march(self.plan_i)
+        if tl is not None:
+            marks["interior_done"].record(main)
+        self.comm.wait_event(boundary_done)
+        with torch.cuda.stream(self.comm):
+            if tl is not None:
+                marks["exchange_start"].record(self.comm)
+            exchange()
+            if tl is not None:
+                marks["exchange_done"].record(self.comm)
+        if tl is not None:
+            marks["boundary_done"] = boundary_done
+            tl.append(marks)
         main.wait_stream(self.comm)
 
 
