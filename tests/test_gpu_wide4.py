@@ -75,6 +75,10 @@ def test_wide4_matches_reference_runs(tm):
     (128, 128, 1, None, None),  # 128-wide: 4 cells per lane, 8-row columns
     (96, 48, 2, 5, 7),         # 5-row columns, segments crossing columns
     (24, 4, 2, None, None),    # 4^3 boxes: every ghost layer from a neighbour box
+    (40, 16, 2, None, None),   # boxes 16 and 8 wide / high: Kernel W2 on non-uniform columns
+    (24, 4, 2, None, 2),       # 216 four-plane columns on 2 CTAs: > 32 segments per CTA (W2's
+                               # descriptor cache overflows to global memory)
+    (64, 32, 2, None, 7),      # W2, segments crossing columns
 ])
 def test_wide4_matches_oracle(tm, n, mgs, steps, rows, nctas):
     w = dataclasses.replace(tm.CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
