@@ -512,6 +512,8 @@ def run_ours(args, w):
                 if runner.fused and runner.use_graph else "eager launches between CUDA events",
                 "eager_launch_ms": eager_ms,
                 "peak_source": peak_src,
+                # north_star quotes "roughly 8 TB/s"; SURVEY.md §8d asks for both figures
+                "frac_vs_nominal_8000_gbs": achieved / 8000.0,
             },
             "unfused_components": {"fill_boundary_ms": fill_ms, "fill_ghost_gbs": fill_gbs,
                                    "ghost_cells": ghost_cells, "heat_step_ms": sweep_ms,
