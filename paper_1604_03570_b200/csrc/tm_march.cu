@@ -132,7 +132,12 @@ __device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensor
 // are exactly the y/z face ghosts a FillBoundary of uold writes, so the step also stores them
 // into uold's ghosts -- the deferred y/z part of the preceding fill_boundary
 // (multifab.fill_boundary), at no extra read.  Other CTAs read only uold's valid cells.
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW = false>
+// HW (half-warp rows, boxes 18..32 wide): lanes 0-15 and 16-31 march two different row groups
+// of the column, 2 cells per lane, so a warp covers 2*RPW rows of a narrow box with the
+// two-cells-per-lane instruction stream instead of one cell per lane (C5's 32-wide boxes:
+// ~61 instructions per cell at one cell per lane against ~40 at two).
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW = false,
+          bool HW = false>
 __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const __grid_constant__ CUtensorMap xmap,
                                                                  const __grid_constant__ CUtensorMap rmap,
@@ -236,8 +241,11 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         const Segment sg = a.segs[REV ? s_end - 1 - si : s_begin + si];
         const tm_block c = a.cols[sg.col];
         const int nk = sg.k1 - sg.k0;
-        const int xi = min(lane * CPL, c.nx - CPL);  // lane's first cell (clamped for idle lanes)
-        const bool lane_on = lane * CPL < c.nx;
+        // this lane's position: x slot lx within its row group, first row row0 of the group
+        const int lx = HW ? (lane & 15) : lane;
+        const int row0 = HW ? warp * 2 * RPW + (lane >> 4) * RPW : warp * RPW;
+        const int xi = min(lx * CPL, c.nx - CPL);  // lane's first cell (clamped for idle lanes)
+        const bool lane_on = lx * CPL < c.nx;
         // output rows: 64-bit row bases + one 32-bit running plane offset
         double *const obase = a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp;
         uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0 + (REV ? nk - 1 : 0)) * st.plane + (int64_t)c.y0 * st.row +
@@ -247,19 +255,19 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         uint32_t roff[RPW];  // smem byte offset of the row's first cell (rows past max_ny clamp; never stored)
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            const int r = warp * RPW + i;
+            const int r = row0 + i;
             on[i] = lane_on && r < c.ny;
             orow[i] = obase + (int64_t)r * st.row;
             roff[i] = (uint32_t)((min(r, max_ny) + 1) * bx + xi + xsh) * 8u;
         }
         // the row after this warp's last row (its y+1 neighbours): clamped to the stage's last
         // row for warps whose rows all lie past the column (values never stored)
-        const uint32_t ypo = (uint32_t)((min(warp * RPW + RPW - 1, max_ny - 1) + 2) * bx + xi + xsh) * 8u;
+        const uint32_t ypo = (uint32_t)((min(row0 + RPW - 1, max_ny - 1) + 2) * bx + xi + xsh) * 8u;
         uint32_t xlo[RPW], xro[RPW];
 #pragma unroll
         for (int i = 0; i < RPW; ++i) {
-            const int r = min(warp * RPW + i, c.ny - 1);
-            const bool left_edge = PACKED && lane == 0;
+            const int r = min(row0 + i, c.ny - 1);
+            const bool left_edge = PACKED && lx == 0;
             const bool right_edge = PACKED && (xi + CPL == c.nx);
             xlo[i] = left_edge ? (uint32_t)(a.xh_off + r) * 8u : roff[i] - 8u;
             xro[i] = right_edge ? (uint32_t)(a.xh_off + max_ny + r) * 8u : roff[i] + (uint32_t)CPL * 8u;
@@ -277,22 +285,20 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         int kz_lo = -1, kz_hi = -1;
         int64_t zoff_lo = 0, zoff_hi = 0;
         if (SCATTER) {
-            if (kYZ && warp == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
+            if (kYZ && row0 == 0 && yl0 == 0 && nb[2] >= 0 && on[0]) {
                 ylo_i = 0;
                 ylo = orow[0] + (int64_t)(nb[2] - c.slot) * st.slot + (int64_t)nyb * st.row;
             }
             const int rl = c.ny - 1;  // last row of the column
-            if (kYZ && yl0 + c.ny == nyb && nb[3] >= 0 && rl / RPW == warp && lane_on) {
-                yhi_i = rl % RPW;
+            if (kYZ && yl0 + c.ny == nyb && nb[3] >= 0 && rl >= row0 && rl < row0 + RPW && lane_on) {
+                yhi_i = rl - row0;
                 yhi = obase + (int64_t)rl * st.row + (int64_t)(nb[3] - c.slot) * st.slot - (int64_t)nyb * st.row;
             }
-            const int xl0 = c.x0 - a.L.xoff + lane * CPL;
+            const int xl0 = c.x0 - a.L.xoff + lx * CPL;
             if (lane_on && xl0 == 0 && nb[0] >= 0)  // our x = 0 cells -> the -x neighbour's right halo
-                xhp = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb + yl0 +
-                      warp * RPW;
+                xhp = a.xh_new + (((int64_t)(nb[0] * a.L.ncomp + comp) * nzb + zl0) * 2 + 1) * nyb + yl0 + row0;
             if (lane_on && xl0 + CPL == c.nx && nb[1] >= 0) {
-                xhp = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb + yl0 +
-                      warp * RPW;
+                xhp = a.xh_new + (((int64_t)(nb[1] * a.L.ncomp + comp) * nzb + zl0) * 2 + 0) * nyb + yl0 + row0;
                 x_right = true;
             }
             if (kYZ && nb[4] >= 0 && zl0 <= 0 && 0 < zl0 + nk) {
@@ -316,10 +322,10 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
         double *gbase = nullptr;
         bool gy_lo = false, gy_hi = false, gz_lo = false, gz_hi = false;
         if (GW) {
-            // koff addresses the column's first row: this warp's rows start warp*RPW rows below
-            gbase = a.gw + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)warp * RPW * st.row;
-            gy_lo = lane_on && warp == 0 && yl0 == 0 && nb[2] >= 0;
-            gy_hi = lane_on && warp * RPW + RPW - 1 == c.ny - 1 && yl0 + c.ny == nyb && nb[3] >= 0;
+            // koff addresses the column's first row: this lane's rows start row0 rows below
+            gbase = a.gw + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)row0 * st.row;
+            gy_lo = lane_on && row0 == 0 && yl0 == 0 && nb[2] >= 0;
+            gy_hi = lane_on && row0 + RPW - 1 == c.ny - 1 && yl0 + c.ny == nyb && nb[3] >= 0;
             gz_lo = zl0 == 0 && nb[4] >= 0;
             gz_hi = zl0 + nk == nzb && nb[5] >= 0;
         }
@@ -800,10 +806,10 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 
 namespace {
 
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW, bool HW = false>
 int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a,
                      int nctas, int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH, GW>;
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH, GW, HW>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -826,9 +832,23 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUte
     return TM_OK;
 }
 
+// TM_HALFWARP=0: boxes 18..32 wide keep one cell per lane (A/B measurements)
+bool halfwarp_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("TM_HALFWARP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false, bool GW = false>
 int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a, int cpl,
-                 int rows, int nctas, int ncomp, size_t smem, cudaStream_t s) {
+                 int rows, int max_nx, int nctas, int ncomp, size_t smem, cudaStream_t s) {
+    if (cpl == 1 && max_nx > 16 && rows <= 32 && halfwarp_enabled()) {  // half-warp row groups, 2 cells per lane
+        if (rows <= 16)
+            return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW, true>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW, true>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    }
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
         if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
@@ -1086,12 +1106,12 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
         p->last_xh_new = xh_new;
     }
     if (halo_mode == TM_HALO_GHOSTS_XH)
-        return launch_march<false, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+        return launch_march<false, true, false>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
     switch (halo_mode) {
         case TM_HALO_GHOSTS:
-            return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+            return launch_march<false, false, false>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
         case TM_HALO_PACKED:
-            return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+            return launch_march<true, false, false>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
         case TM_HALO_FUSED_NBR_GHOSTS:
         case TM_HALO_FUSED_NBR: {
             CUtensorMap cmap, rmap;
@@ -1100,18 +1120,18 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
             rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
             if (rc) return rc;
             if (halo_mode == TM_HALO_FUSED_NBR_GHOSTS)
-                return launch_march<true, true, false, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas,
+                return launch_march<true, true, false, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->max_nx, p->nctas,
                                                                    ncomp_sweep, smem, s);
             if (reverse)
-                return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+                return launch_march<true, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep,
                                                             smem, s);
-            return launch_march<true, true, false, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->nctas, ncomp_sweep,
+            return launch_march<true, true, false, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep,
                                                          smem, s);
         }
         default:
             if (reverse)
-                return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
-            return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->nctas, ncomp_sweep, smem, s);
+                return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
+            return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
     }
 }
 
