@@ -54,10 +54,14 @@ CELLS_PER_PLANE = 1024  # column rows x width per CTA plane; C2 optimum (16 x 64
 
 
 def warps_for(nx: int, rows: int) -> int:
-    """Consumer warps of the march kernel instance (mirrors launch_march)."""
-    if nx > 64:
+    """Consumer warps of the heat / GSRB march kernel instance (mirrors launch_march)."""
+    if nx > 64:  # 4 cells per lane
         return 8 if rows <= 8 else 16
-    return 4 if rows <= 8 else (7 if rows <= 14 else (8 if rows <= 16 else 16))
+    if nx > 32:  # 2 cells per lane
+        return 4 if rows <= 8 else (7 if rows <= 14 else (8 if rows <= 16 else 16))
+    if nx > 16 and rows <= 32:  # heat: half-warp row groups, 2 cells per lane (4 rows per warp)
+        return 4 if rows <= 16 else 8
+    return 4 if rows <= 8 else (8 if rows <= 32 else 16)  # 1 cell per lane
 
 
 def max_rows_for(nx: int, packed: bool) -> int:
