@@ -198,6 +198,16 @@ enum {
 int tm_heat_march(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                   int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode,
                   const double *xh_old, double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream);
+/* The reference-shaped loop's step on the fast path (fill_boundary, level.py:297-323, then
+ * heat_step, kernels.py:174-215, when the fill left uold's y/z face ghosts pending): the
+ * TM_HALO_FUSED_NBR_GHOSTS sweep plus the fill's remaining cells -- uold's edge/corner ghosts,
+ * d_fill_cells = device int64 pairs (dst, src) of element offsets from uold, copied from
+ * uold's valid cells, which this launch does not write -- run by one extra warp per CTA while
+ * the others march: one launch for the whole loop step. */
+int tm_heat_march_fill(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old,
+                       double *xh_new, const int32_t *d_nbr, const int64_t *d_fill_cells, int64_t nfill_cells,
+                       void *stream);
 int tm_march_plan_reset_halos(tm_march_plan *plan);
 
 /* Fused red (0) / black (1) Gauss-Seidel pass of the column march, in place on

@@ -49,6 +49,8 @@ struct MarchArgs {
     double *xh_new;                     // SCATTER: packed x halo of the new field
     double *gw;                         // GW: uold's storage, whose face ghosts the step fills
     const int32_t *nbr;                 // SCATTER: 6 neighbour slots per slot (-x,+x,-y,+y,-z,+z)
+    const int64_t *fcells;              // FILL: (dst, src) element offsets in uold (edge/corner ghosts)
+    int64_t nfcells;
 };
 
 // Plane sequence of a CTA: for each of its segments, planes k0-1 .. k1 (k1-k0+2 planes).
@@ -136,14 +138,18 @@ __device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensor
 // of the column, 2 cells per lane, so a warp covers 2*RPW rows of a narrow box with the
 // two-cells-per-lane instruction stream instead of one cell per lane (C5's 32-wide boxes:
 // ~61 instructions per cell at one cell per lane against ~40 at two).
+// FILL (with GW): one more warp runs the preceding FillBoundary's remaining tags on uold -- its
+// edge/corner ghosts, which the 7-point sweep never reads -- while the other warps march, so the
+// reference-shaped loop (fill_boundary; heat_step) needs no separate copy launch per step.
 template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW = false,
-          bool HW = false>
-__global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
+          bool HW = false, bool FILL = false>
+__global__ void __launch_bounds__((NWARP + 1 + FILL) * 32, NWARP <= 4 ? 3 : (NWARP <= 8 ? 2 : 1)) march_kernel(const __grid_constant__ CUtensorMap map,
                                                                  const __grid_constant__ CUtensorMap xmap,
                                                                  const __grid_constant__ CUtensorMap rmap,
                                                                  MarchArgs a) {
     static_assert(!NBRH || (PACKED && SCATTER), "neighbour-sourced halos belong to the fused mode");
     static_assert(!GW || (NBRH && !REV), "face-ghost writes ride on the forward neighbour-halo step");
+    static_assert(!FILL || GW, "the fill warp rides on the face-ghost-writing step");
     // SCATTER: the epilogue writes the packed x halos of the new field (xh_new); with x halos
     // from the packed buffer and y/z halos from ghost cells (TM_HALO_FUSED_SCATTER) it also
     // writes the y/z face ghosts of unew.  TM_HALO_GHOSTS_XH (!PACKED) writes xh_new only.
@@ -177,6 +183,30 @@ __global__ void __launch_bounds__((NWARP + 1) * 32, NWARP <= 4 ? 3 : (NWARP <= 8
     __syncthreads();
     grid_dep_wait();  // previous step complete: its unew is our uold, its uold our unew
 
+    if (FILL && warp == NWARP + 1) {  // ---------------- fill warp ----------------
+        // one cell per lane: the edge/corner tags are thousands of one-cell rows (a z edge is
+        // one task per plane in Kernel B's row tasks), so lanes take independent cells
+        // (kB cells per lane per trip: every index and value load in flight before the stores)
+        if (blockIdx.y == 0) {  // the list covers every component
+            constexpr int kB = 8;
+            const int64_t stride = (int64_t)gridDim.x * 32;
+            for (int64_t i0 = (int64_t)blockIdx.x * 32 + lane; i0 < a.nfcells; i0 += kB * stride) {
+                longlong2 ds[kB];
+                double v[kB];
+#pragma unroll
+                for (int b = 0; b < kB; ++b) {
+                    const int64_t i = i0 + b * stride;
+                    ds[b] = i < a.nfcells ? reinterpret_cast<const longlong2 *>(a.fcells)[i] : make_longlong2(-1, 0);
+                }
+#pragma unroll
+                for (int b = 0; b < kB; ++b) v[b] = ds[b].x >= 0 ? __ldg(a.gw + ds[b].y) : 0.0;
+#pragma unroll
+                for (int b = 0; b < kB; ++b)
+                    if (ds[b].x >= 0) a.gw[ds[b].x] = v[b];
+            }
+        }
+        return;
+    }
     if (warp == NWARP) {  // ---------------- producer warp ----------------
         if (lane == 0) {
             int p = 0;
@@ -806,10 +836,11 @@ gsrb_march_kernel(const __grid_constant__ CUtensorMap map, const __grid_constant
 
 namespace {
 
-template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW, bool HW = false>
+template <int CPL, int NWARP, int RPW, bool PACKED, bool SCATTER, bool REV, bool NBRH, bool GW, bool HW = false,
+          bool FILL = false>
 int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a,
                      int nctas, int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH, GW, HW>;
+    auto kern = march_kernel<CPL, NWARP, RPW, PACKED, SCATTER, REV, NBRH, GW, HW, FILL>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -818,7 +849,7 @@ int launch_march_one(const CUtensorMap &map, const CUtensorMap &xmap, const CUte
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(nctas, ncomp);
-    cfg.blockDim = dim3((NWARP + 1) * 32);
+    cfg.blockDim = dim3((NWARP + 1 + FILL) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -841,31 +872,31 @@ bool halfwarp_enabled() {
     return on;
 }
 
-template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false, bool GW = false>
+template <bool PACKED, bool SCATTER, bool REV, bool NBRH = false, bool GW = false, bool FILL = false>
 int launch_march(const CUtensorMap &map, const CUtensorMap &xmap, const CUtensorMap &rmap, const MarchArgs &a, int cpl,
                  int rows, int max_nx, int nctas, int ncomp, size_t smem, cudaStream_t s) {
     if (cpl == 1 && max_nx > 16 && rows <= 32 && halfwarp_enabled()) {  // half-warp row groups, 2 cells per lane
         if (rows <= 16)
-            return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW, true>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW, true>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+            return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW, true, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW, true, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
     // rows per CTA: 8 -> 4x2, 16 -> 8x2, 32 -> 16x2, 64 -> 16x4
     if (cpl == 2) {
-        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<2, 4, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 14) return launch_march_one<2, 7, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<2, 8, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 32) return launch_march_one<2, 16, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<2, 16, 4, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
     if (cpl == 4) {  // 4 cells per lane already give ILP: one or two rows per warp
-        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 8) return launch_march_one<4, 8, 1, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        if (rows <= 16) return launch_march_one<4, 16, 1, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+        return launch_march_one<4, 16, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
     }
-    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
-    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV, NBRH, GW>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 8) return launch_march_one<1, 4, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 16) return launch_march_one<1, 8, 2, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    if (rows <= 32) return launch_march_one<1, 8, 4, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
+    return launch_march_one<1, 16, 4, PACKED, SCATTER, REV, NBRH, GW, false, FILL>(map, xmap, rmap, a, nctas, ncomp, smem, s);
 }
 
 
@@ -1012,9 +1043,14 @@ int tm_march_plan_reset_halos(tm_march_plan *p) {
     return TM_OK;
 }
 
-int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
-                  double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode, const double *xh_old,
-                  double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream) {
+}  // extern "C"
+
+namespace {
+
+int heat_march_impl(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
+                    double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode, const double *xh_old,
+                    double *xh_new, const int32_t *d_nbr, int32_t reverse, const int64_t *fill_cells, int64_t nfill,
+                    void *stream) {
     using namespace tmk;
     if (!p) return fail(TM_ERR_INVALID, "tm_heat_march: null plan");
     int rc = check_layout(layout, "tm_heat_march");
@@ -1119,6 +1155,12 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
             if (rc) return rc;
             rc = encode_plane_map(&rmap, L, uold, a.box_x, 1);
             if (rc) return rc;
+            if (halo_mode == TM_HALO_FUSED_NBR_GHOSTS && fill_cells && nfill > 0) {
+                a.fcells = fill_cells;
+                a.nfcells = nfill;
+                return launch_march<true, true, false, true, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny,
+                                                                         p->max_nx, p->nctas, ncomp_sweep, smem, s);
+            }
             if (halo_mode == TM_HALO_FUSED_NBR_GHOSTS)
                 return launch_march<true, true, false, true, true>(cmap, xmap, rmap, a, cpl, p->max_ny, p->max_nx, p->nctas,
                                                                    ncomp_sweep, smem, s);
@@ -1133,6 +1175,28 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
                 return launch_march<true, true, true>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
             return launch_march<true, true, false>(map, xmap, map, a, cpl, p->max_ny, p->max_nx, p->nctas, ncomp_sweep, smem, s);
     }
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
+                  double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode, const double *xh_old,
+                  double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream) {
+    return heat_march_impl(p, layout, uold, unew, ncomp_sweep, dxi0, dxi1, dxi2, dtD, halo_mode, xh_old, xh_new,
+                           d_nbr, reverse, nullptr, 0, stream);
+}
+
+int tm_heat_march_fill(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old,
+                       double *xh_new, const int32_t *d_nbr, const int64_t *d_fill_cells, int64_t nfill_cells,
+                       void *stream) {
+    if (nfill_cells < 0 || (nfill_cells > 0 && !d_fill_cells) ||
+        (reinterpret_cast<uintptr_t>(d_fill_cells) & 15) != 0)
+        return tmk::fail(TM_ERR_INVALID, "tm_heat_march_fill: bad cell list (16-B aligned int64 pairs)");
+    return heat_march_impl(p, layout, uold, unew, ncomp_sweep, dxi0, dxi1, dxi2, dtD, TM_HALO_FUSED_NBR_GHOSTS, xh_old,
+                           xh_new, d_nbr, 0, d_fill_cells, nfill_cells, stream);
 }
 
 int tm_gsrb_march(tm_march_plan *p, const tm_layout *phi_layout, double *phi, const tm_layout *rhs_layout,

@@ -179,9 +179,17 @@ def heat_march(mf_new: MultiFab, mf_old: MultiFab, params, max_rows: int | None 
         _native.check(L.tm_march_plan_reset_halos(plan.handle), "tm_march_plan_reset_halos")
     else:
         plan, mode, xh_old, old_ptr = march_plan(mf_old, False), _native.HALO_GHOSTS_XH, None, mf_old.ptr
-    _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), old_ptr, new_ptr, mf_old.ncomp,
-                                  c[0], c[1], c[2], c[3], mode, xh_old, xh_new.data_ptr(), nbr.data_ptr(), 0,
-                                  mf_old.stream()), "tm_heat_march")
+    edges = mf_old._pending_edges if mode == _native.HALO_FUSED_NBR_GHOSTS else None
+    if edges is not None:  # the fill's edge/corner cells ride on this launch (one extra warp per CTA)
+        cells = mf_old._pending_cells
+        _native.check(L.tm_heat_march_fill(plan.handle, mf_old.layout.to_c(), old_ptr, new_ptr, mf_old.ncomp,
+                                           c[0], c[1], c[2], c[3], xh_old, xh_new.data_ptr(), nbr.data_ptr(),
+                                           cells.data_ptr(), cells.shape[0], mf_old.stream()), "tm_heat_march_fill")
+    else:
+        _native.check(L.tm_heat_march(plan.handle, mf_old.layout.to_c(), old_ptr, new_ptr, mf_old.ncomp,
+                                      c[0], c[1], c[2], c[3], mode, xh_old, xh_new.data_ptr(), nbr.data_ptr(), 0,
+                                      mf_old.stream()), "tm_heat_march")
+    mf_old._pending_edges = None
     mf_old._pending_faces = None
     mf_new._xh_key = mf_new.valid_key()
 

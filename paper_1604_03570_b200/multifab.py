@@ -211,6 +211,8 @@ class MultiFab:
         # next heat_step's sweep writes, and x face ghosts kept as a snapshot of the packed x
         # halos; written into storage ("settled") before anyone can observe them.
         self._pending_faces = None  # copy plan of the y/z face tags
+        self._pending_edges = None  # copy plan of the edge/corner tags (run by the next sweep's fill warp)
+        self._pending_cells = None  # ... and the same cells as a (dst, src) offset list for that warp
         self._vx = None             # packed-halo snapshot holding the x face ghosts
         self._vx_nx = 0
         self._xh_spare = None       # second halo buffer: heat_step writes here while _xh is pinned
@@ -258,9 +260,10 @@ class MultiFab:
         return self._data
 
     def settle(self) -> None:
-        """Write every deferred ghost (y/z faces: one copy launch; x faces: one launch from
-        the packed-halo snapshot) so the storage holds exactly a FillBoundary's ghosts."""
-        if self._pending_faces is None and self._vx is None:
+        """Write every deferred ghost (edges/corners and y/z faces: copy launches; x faces: one
+        launch from the packed-halo snapshot) so the storage holds exactly a FillBoundary's
+        ghosts."""
+        if self._pending_faces is None and self._pending_edges is None and self._vx is None:
             return
         self.settles += 1
         self.settle_faces(count=False)
@@ -271,17 +274,20 @@ class MultiFab:
                           "tm_xh_to_ghosts")
 
     def settle_faces(self, count: bool = True) -> None:
-        """Write pending y/z face ghosts (they are copied from valid cells: before those change)."""
-        pend = self._pending_faces
-        if pend is not None:
-            self._pending_faces = None
-            self.settles += count
-            pend.run(self._data.data_ptr(), self.layout.side(), self._data.data_ptr(), self.layout.side(),
-                     _native.stream_handle(self.device))
+        """Write pending edge/corner and y/z face ghosts (they are copied from valid cells:
+        before those change)."""
+        for name in ("_pending_edges", "_pending_faces"):
+            pend = getattr(self, name)
+            if pend is not None:
+                setattr(self, name, None)
+                self.settles += count
+                pend.run(self._data.data_ptr(), self.layout.side(), self._data.data_ptr(), self.layout.side(),
+                         _native.stream_handle(self.device))
 
     def drop_deferred(self) -> None:
         """A complete FillBoundary is about to rewrite every ghost the deferred ones cover."""
         self._pending_faces = None
+        self._pending_edges = None
         self._vx = None
 
     @property
@@ -672,10 +678,14 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
         # Deferred ghosts are written before anyone can observe them (MultiFab.data / .ptr /
         # FAB views / kernels that touch ghosts settle them), so no caller ever sees a ghost the
         # reference would not.
-        edges, faces, nx = fast
+        edges, faces, nx, cells = fast
         mf.drop_deferred()
-        edges.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
         mf._pending_faces = faces  # y/z faces: written by the next heat_step's sweep
+        if cells is None:
+            edges.run(mf.gptr, mf.layout.side(), mf.ptr, mf.layout.side(), stream)
+        else:
+            mf._pending_edges = edges  # edges/corners: copied by that sweep's fill warp (tm_heat_march_fill)
+            mf._pending_cells = cells
         if _capturing() and not _SNAPSHOTS_IN_CAPTURE[0]:
             # a CUDA graph freezes buffer pointers, and pinning the halo buffer as a snapshot
             # makes the next heat_step write the other one: the pattern repeats only every two
@@ -722,9 +732,10 @@ class snapshots_in_capture:
 
 
 def _xh_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):
-    """(copy plan of the edge/corner tags, copy plan of the y/z face tags, box width) for
-    a one-rank, one-ghost MultiFab on which heat_step runs the neighbour-halo march (the
-    fast path of the reference loop), or None.  Cached per plan and layout."""
+    """(copy plan of the edge/corner tags, copy plan of the y/z face tags, box width, the
+    edge/corner cells as a device offset list or None) for a one-rank, one-ghost MultiFab on
+    which heat_step runs the neighbour-halo march (the fast path of the reference loop), or
+    None.  Cached per plan and layout."""
     key = ("xh_fill",) + _plan_key(mf)
     if key in plan._device:
         return plan._device[key]
@@ -749,10 +760,33 @@ def _xh_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):
         # every box: the plan must fill all of them (periodic / fully covered)
         ny, nz = mf.units[mf.local_units[0]].valid.extents[1:]
         if xfaces == 2 * ny * nz * len(mf.local_units):
-            out = (_native.CopyPlan(local_copy_tags(mf, edges), mf.ncomp),
-                   _native.CopyPlan(local_copy_tags(mf, yz), mf.ncomp), nx)
+            etags = local_copy_tags(mf, edges)
+            out = (_native.CopyPlan(etags, mf.ncomp), _native.CopyPlan(local_copy_tags(mf, yz), mf.ncomp), nx,
+                   _edge_cells(mf, etags))
     plan._device[key] = out
     return out
+
+
+def _edge_cells(mf: MultiFab, tags):
+    """The edge/corner tags as a flat device list of (dst, src) element offsets, one pair per
+    cell and component, for the fill warp of tm_heat_march_fill -- or None when the list would
+    be large (> 64 MB: the tags then run as their own copy launch)."""
+    import torch
+
+    L = mf.layout
+    n = int(sum(int(t["ex"]) * int(t["ey"]) * int(t["ez"]) for t in tags)) * mf.ncomp
+    if n == 0 or 16 * n > 64 * 2 ** 20:
+        return None
+    rel = []
+    for t in tags:
+        x = np.arange(int(t["ex"]), dtype=np.int64)
+        y = np.arange(int(t["ey"]), dtype=np.int64) * L.row
+        z = np.arange(int(t["ez"]), dtype=np.int64) * L.plane
+        c = np.arange(mf.ncomp, dtype=np.int64) * L.comp
+        off = (c[:, None, None, None] + z[None, :, None, None] + y[None, None, :, None] + x).reshape(-1)
+        rel.append(np.stack([off + int(t["dst_off"]), off + int(t["src_off"])], axis=1))
+    cells = np.ascontiguousarray(np.concatenate(rel), dtype=np.int64)
+    return torch.from_numpy(cells).to(mf.device)
 
 
 # --------------------------------------------------------------------------

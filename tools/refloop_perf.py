@@ -33,7 +33,7 @@ def main():
         tm.fill_boundary(b, geom, plan)
         tm.heat_step(a, b, geom, p)
     assert a.xh_current()
-    edges, faces, _ = _xh_fill(a, plan, geom)
+    edges, faces, _, _ = _xh_fill(a, plan, geom)
 
     def edge_part():
         edges.run(a.gptr, a.layout.side(), a.ptr, a.layout.side(), a.stream())
