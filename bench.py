@@ -696,7 +696,8 @@ def config_records(args, peak):
                           "neighbours' valid cells" if r.fused and r.nbr_halos else
                           "fused" if r.fused else "unfused"),
             "reference_loop": {"ms_per_step": ms_ref, "value": cells / (ms_ref * 1e-3),
-                               "how": "fill_boundary (4 ghost layers) + wide4_step (Kernel W2 on ghosts), eager"},
+                               "how": "fill_boundary (4 ghost layers) + wide4_step per step, eager: the fill is "
+                                      "deferred and rides on the step's launch (tm_wide4_march_fill)"},
             "workload": f"wide4 (9-point 8th-order Laplacian, SURVEY §8f row 1): periodic {w.n}^3, "
                         f"max_grid_size {w.max_grid_size} ({len(ba)} boxes), nghost 4, ncomp 1",
             "unit": UNIT,

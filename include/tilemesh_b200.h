@@ -273,6 +273,16 @@ int tm_wide4_march_fused(tm_march_plan *plan, const tm_layout *layout, const dou
 int tm_wide4_march_nbr(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
                        int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
                        double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream);
+/* The reference loop's wide4 step on the fast path (fill_boundary with 4 ghost layers,
+ * level.py:297-323, then wide4_step, kernels.py:218-247, when the fill was deferred): the
+ * tm_wide4_march_nbr step that also writes every 4-deep face ghost of uold as it loads it from
+ * the neighbours, plus the fill's edge/corner cells (d_fill_cells: device int64 (dst, src)
+ * offset pairs from uold, one per run of 4 doubles along x, each 32-B aligned) copied by the
+ * producer warpgroup's idle warps.  Needs nghost == 4. */
+int tm_wide4_march_fill(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                        int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                        double dtD, const int32_t *d_nbr, const int32_t *box_extents, const int64_t *d_fill_cells,
+                        int64_t nfill_cells, void *stream);
 
 /* ---- per-tile heat operations (the reference's building blocks) -------------
  * tm_face_flux replaces heat_flux (kernels.py:86-120 -> compiled.flux_x/y/z,

@@ -50,7 +50,7 @@ EXPORTS = [
     "tm_residual_maxnorm", "tm_reduce_sum", "tm_reduce_minmax",
     "tm_march_plan_create", "tm_march_plan_destroy", "tm_march_plan_reset_halos", "tm_heat_march", "tm_heat_march_fill",
     "tm_gsrb_march", "tm_wide4_march",
-    "tm_wide4_march_fused", "tm_wide4_march_nbr",
+    "tm_wide4_march_fused", "tm_wide4_march_nbr", "tm_wide4_march_fill",
     "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass", "tm_face_flux", "tm_divergence_update",
     "tm_comm_nccl_version", "tm_comm_unique_id", "tm_comm_create", "tm_comm_destroy",
     "tm_exchange_create", "tm_exchange_destroy", "tm_halo_exchange",
@@ -104,6 +104,7 @@ def load():
     L.tm_wide4_march.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp]
     L.tm_wide4_march_fused.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp, vp, vp]
     L.tm_wide4_march_nbr.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp, vp, vp]
+    L.tm_wide4_march_fill.argtypes = [vp, P(tm_layout), vp, vp, i32, vp, f64, f64, f64, f64, vp, vp, vp, i64, vp]
     L.tm_gsrb_split.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, P(tm_layout), vp, vp, vp, vp]
     L.tm_gsrb_merge.argtypes = [P(tm_layout), vp, i32, i32, i32, vp, vp, vp, vp]
     L.tm_gsrb_split_pass.argtypes = [vp, i32, i32, i32, i32, i32, f64, vp, vp, vp, vp, vp]

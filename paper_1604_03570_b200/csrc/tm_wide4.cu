@@ -343,6 +343,9 @@ struct W2Args {
     uint32_t tx_c, tx_h;             // TMA bytes of a centre plane / a window-only plane
     const int32_t *nbr;              // NBR: face neighbours per slot
     int32_t nxv, nyv, nzv;           // NBR: uniform box extents
+    double *gw;                      // GW: uold, whose 4-deep face ghosts the step writes as it loads them
+    const int64_t *fcells;           // GW: (dst, src) offsets in uold of the fill's edge/corner cells
+    int64_t nfcells;
 };
 
 // A CTA's segments as the producer lane needs them, staged in shared memory at kernel
@@ -437,6 +440,68 @@ __device__ __forceinline__ void w2_issue(const W2Args &A, const CUtensorMap *cma
     }
 }
 
+// GW ghost writer (one warp of the producer warpgroup): walks the CTA's planes in the ring's
+// order and, for each stage, copies what the neighbour-halo loads brought in -- the 4 y halo
+// rows and the 4 x halo columns of a centre plane, a whole window-only plane beyond the box --
+// to the same cells of uold's ghost region, then releases the stage like a consumer.  These
+// are exactly the face ghosts a FillBoundary of uold writes (faces whose neighbour is missing
+// were loaded from uold's own ghosts and are skipped).  Inlined: it runs after setmaxnreg.dec (40 regs).
+__device__ __forceinline__ void w2_ghost_writer(const W2Args &A, const double *stages, uint64_t *bars, uint64_t *empty,
+                                             const W2Seg *cache, int s_begin, int s_end, int comp, int lane,
+                                             int which) {
+    using namespace tmk;
+    const Strides st = strides_of(A.L);
+    const int ng = A.L.nghost, bw = A.bw;
+    int32_t cur[2] = {0, 0};
+    int i = 0;
+    W2Seg d = cache[0];
+    uint32_t base = 0;
+    uint32_t total = 0;
+    for (int s = s_begin; s < s_end; ++s) total += (uint32_t)(A.segs[s].k1 - A.segs[s].k0 + 2 * kR);
+    for (uint32_t P = 0; P < total; ++P) {
+        while (P >= base + (uint32_t)(d.nk + 2 * kR)) {
+            base += (uint32_t)(d.nk + 2 * kR);
+            ++i;
+            d = i < kW2SegCache ? cache[i] : w2_seg_global<true>(A, s_begin + i, base);
+        }
+        (void)cur;
+        mbar_wait(&bars[P & (kW4Stages - 1)], (P / kW4Stages) & 1u);
+        if ((int)(P & 1) != which) {  // the other writer's plane: release only
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[P & (kW4Stages - 1)]);
+            continue;
+        }
+        const double *stg = stages + (P & (kW4Stages - 1)) * A.stage_elems;
+        const int q = (int)(P - base), k = d.k0 - kR + q;  // valid z of the plane
+        double *const slot = A.gw + (int64_t)d.slot * st.slot + (int64_t)comp * st.comp + (int64_t)(d.z0 + k) * st.plane;
+        const int nx = A.nxv;
+        auto rows_out = [&](const double *src, int nrows, int y_first) {  // nrows x nx from a stage region
+            if (2 * lane < nx) {  // a row per iteration: lane = cell pair (nx <= 64)
+                double2 *dst = reinterpret_cast<double2 *>(slot + (int64_t)y_first * st.row + d.x0) + lane;
+                const double2 *sp = reinterpret_cast<const double2 *>(src) + lane;
+#pragma unroll 4
+                for (int r = 0; r < nrows; ++r) dst[(int64_t)r * (st.row / 2)] = sp[r * (bw / 2)];
+            }
+        };
+        if (q >= kR && q < d.nk + kR) {  // centre plane: y halo rows, x halo columns
+            if (d.y0 - ng == 0 && d.nb[2] >= 0) rows_out(stg, kR, d.y0 - kR);
+            if (d.y0 - ng + d.ny == A.nyv && d.nb[3] >= 0) rows_out(stg + (kR + d.ny) * bw, kR, d.y0 + d.ny);
+            for (int t = lane; t < 2 * d.ny; t += 32) {  // one 32-B run per row and side
+                const int side = t / d.ny, r = t - side * d.ny;
+                if (d.nb[side] < 0) continue;
+                const double *src = stg + (side ? A.off_xh : A.off_xl) + r * kR;
+                double *dst = slot + (int64_t)(d.y0 + r) * st.row + (side ? d.x0 + nx : d.x0 - kR);
+                reinterpret_cast<double2 *>(dst)[0] = reinterpret_cast<const double2 *>(src)[0];
+                reinterpret_cast<double2 *>(dst)[1] = reinterpret_cast<const double2 *>(src)[1];
+            }
+        } else if ((k < 0 && d.nb[4] >= 0) || (k >= A.nzv && d.nb[5] >= 0)) {  // a ghost plane
+            rows_out(stg + kR * bw, d.ny, d.y0);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[P & (kW4Stages - 1)]);
+    }
+}
+
 // Warp specialisation with register rebalancing: a 9th (producer) warp would put 3 warps on
 // one SM sub-partition and cap every thread at 168 registers, but the consumers' window
 // alone takes 144.  So the block is three warpgroups: warpgroup 2 is the producer (one
@@ -450,7 +515,13 @@ struct IC {
 };
 constexpr int kW2ProdRegs = 40, kW2ConsRegs = 232;
 
-template <bool NBR>
+// GW (with NBR): the step is also the preceding FillBoundary of uold.  Every face halo it loads
+// from a neighbour is exactly a ghost value of uold: two warps of the producer warpgroup copy
+// them from each stage to uold's ghosts (w2_ghost_writer, alternate planes; both release every
+// stage), and the fourth copies the fill's edge/corner cells (which the stencil never reads)
+// from a flat (dst, src) list of 4-double runs.  (Storing them from the consumers' registers put
+// the stores into all nine unrolled plane bodies: 8040 instructions, instruction-cache bound.)
+template <bool NBR, bool GW = false>
 __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
     wide4_col_kernel(const __grid_constant__ CUtensorMap cmap, const __grid_constant__ CUtensorMap ymap,
                      const __grid_constant__ CUtensorMap xmap, W2Args a) {
@@ -478,7 +549,7 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
 #pragma unroll
         for (int s = 0; s < kW4Stages; ++s) {
             mbar_init(&bars[s], 1);
-            mbar_init(&empty[s], kW2Warps);
+            mbar_init(&empty[s], kW2Warps + (GW ? 2 : 0));  // GW: the two ghost writers release stages too
         }
         fence_mbar_init();
         uint32_t base = 0;
@@ -493,6 +564,34 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
 
     if (warp >= kW2Warps) {  // ---------------- producer warpgroup ----------------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kW2ProdRegs));
+        if (GW && (warp == kW2Warps + 1 || warp == kW2Warps + 2)) {  // ghost writers (alternate planes)
+            w2_ghost_writer(a, stages, bars, empty, seg_cache, s_begin, s_end, comp, lane, warp - kW2Warps - 1);
+        } else if (GW && warp == kW2Warps + 3 && blockIdx.y == 0) {  // fill warp (the list covers every component)
+            constexpr int kB = 2;  // entries in flight per lane (40 registers in this warpgroup)
+            const int64_t stride = (int64_t)gridDim.x * 32;
+            for (int64_t i0 = (int64_t)blockIdx.x * 32 + lane; i0 < a.nfcells; i0 += kB * stride) {
+                // entries are runs of 4 doubles along x (32-B aligned: 4-deep ghosts, widths % 4)
+                longlong2 ds[kB];
+                double2 v[kB][2];
+#pragma unroll
+                for (int b = 0; b < kB; ++b) {
+                    const int64_t i = i0 + b * stride;
+                    ds[b] = i < a.nfcells ? reinterpret_cast<const longlong2 *>(a.fcells)[i] : make_longlong2(-1, 0);
+                }
+#pragma unroll
+                for (int b = 0; b < kB; ++b)
+                    if (ds[b].x >= 0) {
+                        v[b][0] = __ldg(reinterpret_cast<const double2 *>(a.gw + ds[b].y));
+                        v[b][1] = __ldg(reinterpret_cast<const double2 *>(a.gw + ds[b].y) + 1);
+                    }
+#pragma unroll
+                for (int b = 0; b < kB; ++b)
+                    if (ds[b].x >= 0) {
+                        reinterpret_cast<double2 *>(a.gw + ds[b].x)[0] = v[b][0];
+                        reinterpret_cast<double2 *>(a.gw + ds[b].x)[1] = v[b][1];
+                    }
+            }
+        }
         if (warp == kW2Warps && lane == 0) {
             uint32_t total = 0;
             for (int s = s_begin; s < s_end; ++s) total += (uint32_t)(a.segs[s].k1 - a.segs[s].k0 + 2 * kR);
@@ -553,6 +652,7 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
             a.out + (int64_t)c.slot * st.slot + (int64_t)comp * st.comp + (int64_t)(c.y0 + r0) * st.row + c.x0 + cx;
         uint32_t koff = (uint32_t)((int64_t)(c.z0 + sg.k0) * st.plane);
 
+
         double w[2 * kR + 1][kW2Rows][2];  // window slot (q % 9) <- segment plane q
         auto load_rows = [&](uint32_t sb, double (&dst)[kW2Rows][2]) {
 #pragma unroll
@@ -587,6 +687,7 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
                             lds_f64x2(sc + (uint32_t)(xo[q] + i * xs[q]), v[2 * q], v[2 * q + 1]);
                         }
                     }
+
                     double sx[2], sy[2], sz[2];
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
@@ -659,10 +760,10 @@ __global__ void __launch_bounds__((kW2Warps + 4) * 32, 1)
     }
 }
 
-template <bool NBR>
+template <bool NBR, bool GW = false>
 int launch_w2(const CUtensorMap &cmap, const CUtensorMap &ymap, const CUtensorMap &xmap, const W2Args &a, int nctas,
               int ncomp, size_t smem, cudaStream_t s) {
-    auto kern = wide4_col_kernel<NBR>;
+    auto kern = wide4_col_kernel<NBR, GW>;
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
@@ -709,7 +810,7 @@ int wide4_dispatch(const CUtensorMap &map, const W4Args &a, const tm_march_plan 
 // neighbours' valid cells, d_box = uniform box extents).  `base` carries the coefficients.
 template <bool NBR>
 int w2_common(const tm_march_plan *p, const tm_layout &L, const double *uold, const W4Args &base, int ncomp_sweep,
-              const int32_t *d_box, cudaStream_t s) {
+              const int32_t *d_box, cudaStream_t s, const int64_t *fill_cells = nullptr, int64_t nfill = -1) {
     using namespace tmk;
     W2Args a{};
     a.cols = p->d_cols;
@@ -755,6 +856,12 @@ int w2_common(const tm_march_plan *p, const tm_layout &L, const double *uold, co
     // stages + full barriers + release counters + 128 B of alignment slack
     const size_t smem = (size_t)kW4Stages * a.stage_elems * sizeof(double) + 2 * kW4Stages * sizeof(uint64_t) + 128;
     if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "wide4 W2: column plane too large for shared memory");
+    if (NBR && nfill >= 0) {  // GW: this step is also uold's FillBoundary
+        a.gw = const_cast<double *>(uold);
+        a.fcells = fill_cells;
+        a.nfcells = nfill;
+        return launch_w2<true, true>(cmap, ymap, xmap, a, p->nctas, ncomp_sweep, smem, s);
+    }
     return launch_w2<NBR>(cmap, ymap, xmap, a, p->nctas, ncomp_sweep, smem, s);
 }
 
@@ -828,9 +935,14 @@ int tm_wide4_march(tm_march_plan *p, const tm_layout *layout, const double *uold
                         stream, "tm_wide4_march");
 }
 
-int tm_wide4_march_nbr(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
-                       int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
-                       double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream) {
+}  // extern "C"
+
+namespace {
+
+int wide4_nbr_impl(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                   int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                   double dtD, const int32_t *d_nbr, const int32_t *box_extents, const int64_t *fill_cells,
+                   int64_t nfill, void *stream) {
     using namespace tmk;
     if (!p) return fail(TM_ERR_INVALID, "tm_wide4_march_nbr: null plan");
     int rc = check_layout(layout, "tm_wide4_march_nbr");
@@ -863,7 +975,31 @@ int tm_wide4_march_nbr(tm_march_plan *p, const tm_layout *layout, const double *
     a.d2 = dxi2_2;
     a.dtD = dtD;
     a.nbr = d_nbr;
-    return w2_common<true>(p, L, uold, a, ncomp_sweep, box_extents, as_stream(stream));
+    return w2_common<true>(p, L, uold, a, ncomp_sweep, box_extents, as_stream(stream), fill_cells, nfill);
+}
+
+}  // namespace
+
+extern "C" {
+
+int tm_wide4_march_nbr(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                       double dtD, const int32_t *d_nbr, const int32_t *box_extents, void *stream) {
+    return wide4_nbr_impl(p, layout, uold, unew, ncomp_sweep, coeffs5, dxi2_0, dxi2_1, dxi2_2, dtD, d_nbr,
+                          box_extents, nullptr, -1, stream);
+}
+
+int tm_wide4_march_fill(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                        int32_t ncomp_sweep, const double *coeffs5, double dxi2_0, double dxi2_1, double dxi2_2,
+                        double dtD, const int32_t *d_nbr, const int32_t *box_extents, const int64_t *d_fill_cells,
+                        int64_t nfill_cells, void *stream) {
+    if (!layout || layout->nghost != kR)
+        return tmk::fail(TM_ERR_INVALID, "tm_wide4_march_fill: needs exactly 4 ghost layers (it writes all of them)");
+    if (nfill_cells < 0 || (nfill_cells > 0 && !d_fill_cells) ||
+        (reinterpret_cast<uintptr_t>(d_fill_cells) & 15) != 0)
+        return tmk::fail(TM_ERR_INVALID, "tm_wide4_march_fill: bad cell list (16-B aligned int64 pairs)");
+    return wide4_nbr_impl(p, layout, uold, unew, ncomp_sweep, coeffs5, dxi2_0, dxi2_1, dxi2_2, dtD, d_nbr,
+                          box_extents, d_fill_cells, nfill_cells, stream);
 }
 
 int tm_wide4_march_fused(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,

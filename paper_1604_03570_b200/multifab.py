@@ -213,6 +213,7 @@ class MultiFab:
         self._pending_faces = None  # copy plan of the y/z face tags
         self._pending_edges = None  # copy plan of the edge/corner tags (run by the next sweep's fill warp)
         self._pending_cells = None  # ... and the same cells as a (dst, src) offset list for that warp
+        self._w4_deferred = False   # the pending ghosts are a whole 4-deep fill (wide4 fast path)
         self._vx = None             # packed-halo snapshot holding the x face ghosts
         self._vx_nx = 0
         self._xh_spare = None       # second halo buffer: heat_step writes here while _xh is pinned
@@ -283,11 +284,13 @@ class MultiFab:
                 self.settles += count
                 pend.run(self._data.data_ptr(), self.layout.side(), self._data.data_ptr(), self.layout.side(),
                          _native.stream_handle(self.device))
+        self._w4_deferred = False
 
     def drop_deferred(self) -> None:
         """A complete FillBoundary is about to rewrite every ghost the deferred ones cover."""
         self._pending_faces = None
         self._pending_edges = None
+        self._w4_deferred = False
         self._vx = None
 
     @property
@@ -670,6 +673,18 @@ def fill_boundary(mf: MultiFab, geom: Geometry, plan: FillPlan | None = None, wo
             mf._plans[("fill", geom)] = plan
     stream = mf.stream()
     fast = _xh_fill(mf, plan, geom) if mf.xh_current() else None
+    w4 = _w4_fill(mf, plan, geom) if fast is None and mf.nghost == 4 else None
+    if w4 is not None:
+        # wide4 reference-loop fast path: every ghost is deferred; the next wide4_step writes the
+        # face ghosts as it loads them from the neighbours and copies the edge/corner cells in the
+        # same launch (tm_wide4_march_fill).  Anything observing or overwriting the field first
+        # settles them (one copy launch each for faces and edges), as for heat_step's path.
+        faces, edges, cells = w4
+        mf.drop_deferred()
+        mf._pending_faces, mf._pending_edges, mf._pending_cells = faces, edges, cells
+        mf._w4_deferred = True
+        mf._fill_key = mf.valid_key()
+        return
     if fast is not None:
         # Reference-loop fast path.  The packed x halos the last heat_step wrote are current,
         # so the next heat_step can run the neighbour-halo march, whose y/z halo loads ARE this
@@ -767,19 +782,50 @@ def _xh_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):
     return out
 
 
-def _edge_cells(mf: MultiFab, tags):
+def _w4_fill(mf: MultiFab, plan: FillPlan, geom: Geometry):
+    """(copy plan of the face tags, copy plan of the edge/corner tags, the edge/corner cells as
+    a device offset list) for a one-rank MultiFab with exactly 4 ghost layers on which
+    wide4_step can run Kernel W2 with neighbour-sourced halos (the wide4 reference loop's fast
+    path), or None.  Cached per plan and layout."""
+    key = ("w4_fill",) + _plan_key(mf)
+    if key in plan._device:
+        return plan._device[key]
+    out = None
+    if mf.nghost == 4 and mf.dm.nranks == 1 and mf.ncomp == 1 and mf.local_units:
+        from .march import fusable
+        from .wide4 import w2_nbr_eligible
+
+        if fusable(mf, geom) and w2_nbr_eligible(mf):
+            faces, edges = [], []
+            for t in plan.tags:
+                v, d = mf.units[t.dst_unit].valid, t.dst_box
+                out_dims = [k for k in range(3) if d.lo[k] < v.lo[k] or d.hi[k] > v.hi[k]]
+                (faces if len(out_dims) == 1 else edges).append(t)
+            etags = local_copy_tags(mf, edges)
+            cells = _edge_cells(mf, etags, chunk=4)
+            if cells is not None:
+                out = (_native.CopyPlan(local_copy_tags(mf, faces), mf.ncomp), _native.CopyPlan(etags, mf.ncomp),
+                       cells)
+    plan._device[key] = out
+    return out
+
+
+def _edge_cells(mf: MultiFab, tags, chunk: int = 1):
     """The edge/corner tags as a flat device list of (dst, src) element offsets, one pair per
-    cell and component, for the fill warp of tm_heat_march_fill -- or None when the list would
-    be large (> 64 MB: the tags then run as their own copy launch)."""
+    run of ``chunk`` cells along x (and component), for the fill warps of tm_heat_march_fill
+    (chunk 1) / tm_wide4_march_fill (chunk 4: runs of 4 doubles, 32-B aligned) -- or None when a
+    tag's x extent or offsets do not fit the chunk or the list would be large (> 64 MB)."""
     import torch
 
     L = mf.layout
-    n = int(sum(int(t["ex"]) * int(t["ey"]) * int(t["ez"]) for t in tags)) * mf.ncomp
+    if any(int(t["ex"]) % chunk or int(t["dst_off"]) % chunk or int(t["src_off"]) % chunk for t in tags):
+        return None
+    n = int(sum(int(t["ex"]) * int(t["ey"]) * int(t["ez"]) for t in tags)) * mf.ncomp // chunk
     if n == 0 or 16 * n > 64 * 2 ** 20:
         return None
     rel = []
     for t in tags:
-        x = np.arange(int(t["ex"]), dtype=np.int64)
+        x = np.arange(0, int(t["ex"]), chunk, dtype=np.int64)
         y = np.arange(int(t["ey"]), dtype=np.int64) * L.row
         z = np.arange(int(t["ez"]), dtype=np.int64) * L.plane
         c = np.arange(mf.ncomp, dtype=np.int64) * L.comp

@@ -127,6 +127,53 @@ def wide4_plan(mf: MultiFab, max_rows: int | None = None, nctas: int | None = No
     return plan
 
 
+def w2_nbr_eligible(mf: MultiFab) -> bool:
+    """Uniform boxes that Kernel W2 runs with neighbour-sourced halos: width a multiple of 4
+    (<= 64) and every box cut into columns of one height."""
+    from .march import _even_chunks
+
+    ext = {mf.units[u].valid.extents for u in mf.local_units}
+    if len(ext) != 1 or _w2_rows(mf) is None:
+        return False
+    nx, ny, nz = next(iter(ext))
+    return nx % 4 == 0 and min(nx, ny, nz) >= 2 * RADIUS and len({sz for _, sz in _even_chunks(ny, W2_ROWS)}) == 1
+
+
+def _nbr_context(mf: MultiFab, geom: Geometry):
+    """(device face-neighbour table, box extents) of a W2-NBR layout, cached per geometry."""
+    import torch
+
+    from .march import face_neighbors
+
+    key = ("w4_nbr", geom)
+    ctx = mf._plans.get(key)
+    if ctx is None:
+        nbr = torch.as_tensor(face_neighbors(mf, geom).reshape(-1), dtype=torch.int32, device=mf.device)
+        box = (ctypes.c_int32 * 3)(*mf.units[mf.local_units[0]].valid.extents)
+        ctx = (nbr, box)
+        mf._plans[key] = ctx
+    return ctx
+
+
+def _launch_fill(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: float, dt: float,
+                 coeffs: StencilCoeffs8 | None) -> None:
+    """The wide4 step of the reference loop's fast path: the deferred fill of mf_old and the
+    step in one launch (tm_wide4_march_fill)."""
+    c = coeffs if coeffs is not None else derive_coeffs8()
+    dxi2 = tuple(1.0 / d ** 2 for d in geom.dx)
+    plan = wide4_plan(mf_old)
+    nbr, box = _nbr_context(mf_old, geom)
+    cells = mf_old._pending_cells
+    cbuf = (ctypes.c_double * 5)(c.c0, c.c1, c.c2, c.c3, c.c4)
+    new_ptr = mf_new.wptr
+    _native.check(_native.load().tm_wide4_march_fill(
+        plan.handle, mf_old.layout.to_c(), mf_old._data.data_ptr(), new_ptr, 1, ctypes.cast(cbuf, ctypes.c_void_p),
+        dxi2[0], dxi2[1], dxi2[2], diffusivity * dt, nbr.data_ptr(), box, cells.data_ptr(), cells.shape[0],
+        mf_old.stream()), "tm_wide4_march_fill")
+    mf_old._pending_faces = mf_old._pending_edges = mf_old._pending_cells = None
+    mf_old._w4_deferred = False
+
+
 def _check(mf_new: MultiFab, mf_old: MultiFab) -> None:
     if mf_new.ncomp != 1 or mf_old.ncomp != 1:
         raise ValueError("stencil kernels operate on single-component MultiFabs")
@@ -134,7 +181,7 @@ def _check(mf_new: MultiFab, mf_old: MultiFab) -> None:
         raise ValueError("wide4 kernel requires nghost >= 4")
     if not mf_new.same_layout(mf_old):
         raise ValueError("mf_new and mf_old must share box layout, ncomp, nghost and distribution")
-    if mf_new.data.data_ptr() == mf_old.data.data_ptr():
+    if mf_new._data.data_ptr() == mf_old._data.data_ptr():  # (not .data: that settles deferred ghosts)
         raise ValueError("wide4_step needs distinct old/new MultiFabs (double buffering)")
 
 
@@ -160,6 +207,9 @@ def wide4_step(mf_new: MultiFab, mf_old: MultiFab, geom: Geometry, diffusivity: 
     the tiling, reference test_kernels.py:360-368): the device
     decomposition is the persistent column march."""
     _check(mf_new, mf_old)
+    if mf_old._w4_deferred and mf_old._pending_faces is not None:
+        _launch_fill(mf_new, mf_old, geom, diffusivity, dt, coeffs)  # the fill rides on this launch
+        return
     _launch(mf_new, mf_old, geom, diffusivity, dt, coeffs)
 
 

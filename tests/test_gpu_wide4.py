@@ -264,3 +264,59 @@ def test_fused_wide4_eligibility(tm):
     geom23 = tm.Geometry(dom23, (True, True, True), (1.0 / 23,) * 3)
     ragged = tm.MultiFab(tm.BoxArray.chop(dom23, 10), 1, 4)  # 8, 8, 7 cells: not uniform
     assert not tm.Wide4Runner(ragged, geom23, 1.0, 1e-6).fused
+
+
+@pytest.mark.parametrize("n,mgs,steps", [(128, 64, 4), (96, 32, 5), (64, 16, 3)])
+def test_wide4_reference_loop_fast_path(tm, n, mgs, steps):
+    """fill_boundary (4 layers) + wide4_step on a W2-eligible layout: the fill is deferred and
+    rides on the step's launch (tm_wide4_march_fill: face ghosts written as loaded, edge/corner
+    cells by the producer warpgroup's idle warps).  Fields vs the oracle; the ghosts a caller
+    observes between the calls equal a regular FillBoundary's."""
+    w = dataclasses.replace(tm.CONFIGS["C1"].scaled(n, mgs, steps), nghost=4)
+    glob = tm.make_init(w)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, w.max_grid_size)
+    dt = tm.wide4_stable_dt(1.0, (w.dx,) * 3)
+    coeffs = tm.derive_coeffs8()
+    old = tm.MultiFab(ba, 1, 4)
+    old.from_global(glob)
+    new = old.clone_empty()
+    plan = tm.build_fill_plan(old, geom)
+    for s in range(steps):
+        tm.fill_boundary(old, geom, plan)
+        assert old._w4_deferred, "the wide4 fill fast path was not taken"
+        if s == 1:  # observe the deferred ghosts: they must be a regular fill's
+            ref = tm.MultiFab(ba, 1, 4)
+            ref.from_global(old.to_global())
+            ref.drop_deferred()
+            copy, _ = __import__("paper_1604_03570_b200.multifab", fromlist=["_device_fill"])._device_fill(ref, plan)
+            copy.run(ref.gptr, ref.layout.side(), ref.ptr, ref.layout.side(), ref.stream())
+            for u in old.local_units:
+                fa, fb = old.fab(u), ref.fab(u)  # .fab views settle the deferred ghosts first
+                assert np.array_equal(fa.view(fa.abox, 0, 1).cpu().numpy(), fb.view(fb.abox, 0, 1).cpu().numpy())
+            assert not old._w4_deferred
+        settles = old.settles
+        tm.wide4_step(new, old, geom, 1.0, dt, coeffs=coeffs)
+        if s != 1:  # the fill rode on the step's launch: nothing was settled by a copy launch
+            assert old.settles == settles and old._pending_faces is None
+        if s == 2:  # the step wrote old's ghosts itself (nothing pending): they are a fill's
+            assert old._pending_faces is None and not old._w4_deferred
+            ref = tm.MultiFab(ba, 1, 4)
+            ref.from_global(old.to_global())
+            tm.fill_boundary(ref, geom, plan)
+            for u in old.local_units:
+                fa, fb = old.fab(u), ref.fab(u)
+                assert np.array_equal(fa.view(fa.abox, 0, 1).cpu().numpy(), fb.view(fb.abox, 0, 1).cpu().numpy())
+        old, new = new, old
+    want = orc.wide4_periodic(glob[0], steps, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
+    assert np.array_equal(old.to_global().cpu().numpy()[0], want)
+    # after the last step the field the loop read last carries a whole fill, written in-kernel
+    tm.fill_boundary(old, geom, plan)
+    fin = old.data.cpu().numpy()  # settles
+    ref = tm.MultiFab(ba, 1, 4)
+    ref.from_global(old.to_global())
+    tm.fill_boundary(ref, geom, plan)
+    for u in old.local_units:
+        fa, fb = old.fab(u), ref.fab(u)
+        assert np.array_equal(fa.view(fa.abox, 0, 1).cpu().numpy(), fb.view(fb.abox, 0, 1).cpu().numpy())
+    assert fin.shape == old._data.shape
