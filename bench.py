@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-pipeline", action="store_true", help="skip the two-jobs-in-flight e2e variant")
     ap.add_argument("--configs", default="C3,C4,C5",
                     help="other BASELINE configs measured after the headline at N=1 ('' to skip)")
+    ap.add_argument("--exchange", choices=["auto", "nccl", "peer"], default="auto",
+                    help="multi-GPU halos: NCCL messages, or peer: the march reads other ranks' faces over "
+                         "NVLink (auto: peer when every rank can map its peers and a short run matches NCCL)")
     ap.add_argument("--hot-steps", type=int, default=2000,
                     help="untimed steps run right before the timed region (keeps clocks up)")
     return ap.parse_args()
@@ -301,8 +304,7 @@ def run_ours(args, w):
     params = tm.HeatParams.stable(1.0, geom.dx)
     plan = tm.build_fill_plan(mf, geom)
     sched = tm.build_schedule(mf, w.tile_size)
-    runner = HeatRunner(mf, geom, params, sched, plan, use_graph=not args.no_graph, zmerge=args.zmerge,
-                        fused=False if args.unfused else None)
+    runner, peer_check = make_runner(args, HeatRunner, mf, geom, params, sched, plan, world, dev)
     local_cells = sum(ba[u].ncells for u in mf.local_units) * w.ncomp
     total_cells = w.cells * w.ncomp
 
@@ -365,7 +367,10 @@ def run_ours(args, w):
         kern_ms = timed(fused_step)
         kern_name = ("march_kernel<PACKED,SCATTER,NBRH> (tm_heat_march TM_HALO_FUSED_NBR: sweep + fused "
                      "face-halo exchange)")
-        if world > 1:
+        if world > 1 and runner.exchange == "peer":
+            kern_name += (" with remote faces TMA-loaded from the peers' storage over NVLink (tm_heat_march_peer)"
+                          " + tm_peer_barrier")
+        elif world > 1:
             kern_name += " + NCCL halo exchange of remote faces"
     fill_ms = timed(lambda o, n: tm.fill_boundary(o, geom, plan))
     sweep_ms = timed(lambda o, n: tm.heat_step(n, o, geom, params, sched, zmerge=args.zmerge))
@@ -493,7 +498,10 @@ def run_ours(args, w):
                 "step": "FillBoundary + heat sweep over all boxes",
                 "l2": f"inputs larger than L2: {2 * local_cells * 8 / 1e6:.0f} MB streamed per step per GPU "
                       f"vs 126 MB L2",
-                "parallelism": f"dm{world} (contiguous box slabs, one process per GPU, NCCL halo exchange)",
+                "parallelism": f"dm{world} (contiguous box slabs, one process per GPU, " + (
+                    "peer halos: faces read over NVLink inside the march, one device barrier per step)"
+                    if runner.exchange == "peer" else "NCCL halo exchange)"),
+                "exchange": runner.exchange, "peer_check": peer_check,
                 "cuda_graph": runner.use_graph, "zmerge": args.zmerge,
                 "step_impl": ("fused: one persistent column-march launch per step; y/z halos read from the face "
                               "neighbours' valid cells, x halos from packed buffers the previous step's epilogue "
@@ -537,6 +545,58 @@ def run_ours(args, w):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def make_runner(args, HeatRunner, mf, geom, params, sched, plan, world, dev):
+    """The bench runner.  Multi-GPU with ``--exchange auto|peer``: the peer path (peer.py) when
+    every rank can map its peers' memory; under ``auto`` it is kept only if 4 steps of it give
+    the same bytes as 4 steps of the NCCL path from the same state on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    kw = dict(use_graph=not args.no_graph, zmerge=args.zmerge, fused=False if args.unfused else None)
+    if world == 1 or args.unfused or args.exchange == "nccl":
+        return HeatRunner(mf, geom, params, sched, plan, **kw), None
+    from paper_1604_03570_b200.peer import peer_face_table
+
+    ok = 1
+    why = "ok"
+    try:
+        peer_face_table(mf, geom)
+        n = torch.cuda.device_count()
+        if not all(torch.cuda.can_device_access_peer(dev.index, j) for j in range(n) if j != dev.index):
+            ok, why = 0, "no peer access between the GPUs"
+    except ValueError as e:
+        ok, why = 0, str(e)
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) != 1:
+        if args.exchange == "peer":
+            raise SystemExit(f"bench.py: --exchange peer not possible: {why}")
+        return HeatRunner(mf, geom, params, sched, plan, **kw), {"used": False, "why": why}
+    if args.exchange == "peer":
+        return HeatRunner(mf, geom, params, sched, plan, exchange="peer", **kw), {"used": True, "checked": False}
+    # auto: same 4 steps through both paths (copies of the initial state), bytes compared on every rank
+    ref_mf = mf.clone_empty()
+    ref_mf.data.copy_(mf.data)
+    ref = HeatRunner(ref_mf, geom, params, sched, plan, use_graph=False)
+    want = ref.advance(4).data.clone()
+    ref.close()
+    del ref, ref_mf
+    probe_mf = mf.clone_empty()
+    probe_mf.data.copy_(mf.data)
+    probe = HeatRunner(probe_mf, geom, params, sched, plan, exchange="peer", use_graph=False)
+    same = torch.equal(probe.advance(4).data.view(torch.int64), want.view(torch.int64))
+    torch.cuda.synchronize()
+    dist.barrier()
+    probe.fh.close()
+    del probe, probe_mf, want
+    flag = torch.tensor([1 if same else 0], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) != 1:
+        return HeatRunner(mf, geom, params, sched, plan, **kw), {"used": False, "why": "4-step check vs NCCL differed"}
+    runner = HeatRunner(mf, geom, params, sched, plan, exchange="peer", **kw)
+    return runner, {"used": True, "checked": "4 steps bit-identical to the NCCL path on every rank"}
 
 
 def pipelined_e2e(runner, HeatRunner, mf, geom, params, sched, plan, args, host_in, slab, job_steps, host_csum,

@@ -51,7 +51,7 @@ extern "C" {
 #define TM_ERR_CUDA 2    /* CUDA runtime / driver failure */
 #define TM_ERR_NOMEM 3
 
-#define TM_ABI_VERSION 3
+#define TM_ABI_VERSION 4
 
 typedef struct tm_layout {
     int64_t nslots; /* FAB slots in the allocation */
@@ -336,6 +336,63 @@ int tm_exchange_create(tm_comm *comm, int32_t npeers, const int32_t *peers, cons
                        tm_exchange **out);
 int tm_exchange_destroy(tm_exchange *x);
 int tm_halo_exchange(tm_exchange *x, const double *sendbuf, double *recvbuf, void *stream);
+
+/* ---- peer (NVLink / NVSwitch) halos: the exchange fused into the sweep -----
+ * Replaces the remote half of fill_boundary (level.py:297-323) together with
+ * the heat_step that follows it (kernels.py:174-215) when the GPUs of the job
+ * can map each other's memory: the march kernel (TM_HALO_FUSED_NBR) TMA-loads
+ * the y/z halo planes and rows of a box whose face neighbour lives on another
+ * rank straight from that rank's valid cells over NVLink, plane by plane while
+ * it computes.  No pack, no message, no unpack; a step is one march launch
+ * plus one tm_peer_barrier.  BoxLib's remote ghost traffic: PAPER.md:549-556.
+ *
+ * Neighbour table entries (d_nbr, 6 per slot) for faces on another rank:
+ * TM_NBR_PEER(p, s) = -3 - (p * 2^24 + s): slot s of peer p of the current
+ * peer set (p < TM_MAX_PEERS, s < 2^24).  Only y and z faces may be peers (x
+ * neighbours stay on the rank: the packed x halos are written locally).
+ *
+ * tm_ipc_export: a CUDA IPC handle (64 bytes) of the allocation holding ptr
+ * and ptr's byte offset inside it.  tm_ipc_open (in another process) maps it
+ * and returns the peer's ptr; tm_ipc_close unmaps (pass the pointer
+ * tm_ipc_open returned).
+ *
+ * tm_march_plan_set_peers: peer set `set` (< TM_PEER_SETS) = npeers fields,
+ * peer p's storage at peer_base[p] with the caller's layout except nslots =
+ * peer_nslots[p] (every rank of a job shares pitch / ny / nz / xoff / ncomp /
+ * nghost).  Encodes the peers' TMA maps once into device memory; call at
+ * setup, not inside a graph capture.  A double-buffered pair uses set 0 for
+ * the peers' first field and set 1 for their second.
+ *
+ * tm_heat_march_peer: tm_heat_march in TM_HALO_FUSED_NBR with peer faces read
+ * through `set`.  The peers' uold must be complete and the peers must have
+ * finished reading the field unew overwrites (their previous step): order the
+ * ranks with one tm_peer_barrier between consecutive steps.
+ *
+ * tm_peer_barrier: device-side barrier of this rank with `npeers` peers on
+ * `stream`, graph-capturable.  inbox = this rank's TM_MAX_RANKS uint64
+ * counters (device memory, zeroed once; peers hold it through IPC),
+ * peer_inbox[i] = rank peer_ranks[i]'s inbox as mapped here (device array of
+ * pointers), epoch = this rank's uint64 epoch counter (device).  One thread
+ * per peer adds 1 to peer_inbox[i][my_rank] (release, system scope), then
+ * waits until inbox[peer_ranks[i]] reaches the new epoch (acquire, system
+ * scope).  A wait that exceeds timeout_ns sets *status (device int32) to 1
+ * and returns instead of hanging.  Only for ranks on DIFFERENT GPUs: ranks
+ * sharing a GPU must be ordered by the host (B200_PROFILING.md: kernels that
+ * wait on one another must not share a device). */
+#define TM_MAX_PEERS 8
+#define TM_PEER_SETS 4
+#define TM_MAX_RANKS 64
+#define TM_NBR_PEER(p, s) (-3 - (int32_t)(((int32_t)(p) << 24) + (int32_t)(s)))
+int tm_ipc_export(const void *ptr, uint8_t *handle64, int64_t *offset);
+int tm_ipc_open(const uint8_t *handle64, int64_t offset, void **ptr);
+int tm_ipc_close(void *ptr, int64_t offset);
+int tm_march_plan_set_peers(tm_march_plan *plan, int32_t set, const tm_layout *layout, int32_t npeers,
+                            const double *const *peer_base, const int64_t *peer_nslots);
+int tm_heat_march_peer(tm_march_plan *plan, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old,
+                       double *xh_new, const int32_t *d_nbr, int32_t set, int32_t reverse, void *stream);
+int tm_peer_barrier(uint64_t *inbox, uint64_t *const *peer_inbox, const int32_t *peer_ranks, int32_t npeers,
+                    int32_t my_rank, uint64_t *epoch, int32_t *status, int64_t timeout_ns, void *stream);
 
 #ifdef __cplusplus
 }

@@ -20,10 +20,19 @@ LIB_PATH = os.environ.get("TILEMESH_LIB") or os.path.join(HERE, "libtilemesh_b20
 TM_OK = 0
 TM_ERR_INVALID = 1
 TM_ERR_CUDA = 2
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 # halo_mode of tm_heat_march (include/tilemesh_b200.h)
 HALO_GHOSTS, HALO_PACKED, HALO_FUSED_SCATTER, HALO_FUSED_NBR, HALO_GHOSTS_XH, HALO_FUSED_NBR_GHOSTS = 0, 1, 2, 3, 4, 5
+# peer halos (include/tilemesh_b200.h): neighbour-table code of slot s on peer p of a peer set
+MAX_PEERS, PEER_SETS, MAX_RANKS = 8, 4, 64
+
+
+def nbr_peer(p: int, s: int) -> int:
+    """TM_NBR_PEER(p, s)."""
+    if not (0 <= p < MAX_PEERS and 0 <= s < (1 << 24)):
+        raise ValueError(f"peer face ({p}, {s}) out of range")
+    return -3 - ((p << 24) + s)
 
 
 class tm_layout(ctypes.Structure):
@@ -54,6 +63,8 @@ EXPORTS = [
     "tm_gsrb_split", "tm_gsrb_merge", "tm_gsrb_split_pass", "tm_face_flux", "tm_divergence_update",
     "tm_comm_nccl_version", "tm_comm_unique_id", "tm_comm_create", "tm_comm_destroy",
     "tm_exchange_create", "tm_exchange_destroy", "tm_halo_exchange",
+    "tm_ipc_export", "tm_ipc_open", "tm_ipc_close", "tm_march_plan_set_peers", "tm_heat_march_peer",
+    "tm_peer_barrier",
 ]
 
 _lib = None
@@ -118,6 +129,12 @@ def load():
     L.tm_exchange_create.argtypes = [vp, i32, vp, vp, vp, vp, vp, P(vp)]
     L.tm_exchange_destroy.argtypes = [vp]
     L.tm_halo_exchange.argtypes = [vp, vp, vp, vp]
+    L.tm_ipc_export.argtypes = [vp, ctypes.c_char_p, P(i64)]
+    L.tm_ipc_open.argtypes = [ctypes.c_char_p, i64, P(vp)]
+    L.tm_ipc_close.argtypes = [vp, i64]
+    L.tm_march_plan_set_peers.argtypes = [vp, i32, P(tm_layout), i32, P(vp), P(i64)]
+    L.tm_heat_march_peer.argtypes = [vp, P(tm_layout), vp, vp, i32, f64, f64, f64, f64, vp, vp, vp, i32, i32, vp]
+    L.tm_peer_barrier.argtypes = [vp, vp, vp, i32, i32, vp, vp, i64, vp]
     for name in EXPORTS:
         if name not in ("tm_last_error", "tm_abi_version", "tm_copy_plan_elements"):
             getattr(L, name).restype = ctypes.c_int

@@ -22,6 +22,7 @@
 //
 // Arithmetic is identical to Kernel A (reference flux form, FMA-free).
 #include <algorithm>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -51,6 +52,7 @@ struct MarchArgs {
     const int32_t *nbr;                 // SCATTER: 6 neighbour slots per slot (-x,+x,-y,+y,-z,+z)
     const int64_t *fcells;              // FILL: (dst, src) element offsets in uold (edge/corner ghosts)
     int64_t nfcells;
+    const CUtensorMap *pmaps;           // NBRH peer faces: [TM_MAX_PEERS][2] maps of the peer set (or null)
 };
 
 // Plane sequence of a CTA: for each of its segments, planes k0-1 .. k1 (k1-k0+2 planes).
@@ -95,6 +97,28 @@ struct NbrFaces {
     bool top, bot;               // the column's first / last row is a box face
 };
 
+// A face's source: local slot v >= 0 (the field's own maps) or a peer face v <= -3
+// (TM_NBR_PEER: slot of peer p, read through peer p's maps over NVLink); -1 / -2 (none,
+// remote via the halo exchange): no source, the halo comes from our own ghost cells.
+__device__ __forceinline__ bool nbr_src(int32_t v, const MarchArgs &a, const CUtensorMap *map,
+                                        const CUtensorMap *rmap, int &slot, const CUtensorMap *&m,
+                                        const CUtensorMap *&r) {
+    if (v >= 0) {
+        slot = v;
+        m = map;
+        r = rmap;
+        return true;
+    }
+    if (v <= -3) {
+        const int q = -3 - v;
+        slot = q & 0xffffff;
+        m = a.pmaps + 2 * (q >> 24);
+        r = m + 1;
+        return true;
+    }
+    return false;
+}
+
 __device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensorMap *rmap, const CUtensorMap *xmap,
                                           const MarchArgs &a, double *stage, uint64_t *bar, const tm_block &c,
                                           const NbrFaces &f, int comp, int z, uint32_t tx_bytes) {
@@ -102,26 +126,31 @@ __device__ __forceinline__ void issue_nbr(const CUtensorMap *map, const CUtensor
     const int nc = a.L.ncomp, g = a.L.nghost;
     const int w = c.slot * nc + comp;
     const int zl = z - g;  // valid z index of the plane
-    int ws = w, zs = z;
-    if (zl < 0 && f.zlo >= 0) {
-        ws = f.zlo * nc + comp;
+    int ws = w, zs = z, s = 0;
+    const CUtensorMap *zm = map, *zr = rmap, *m = map, *r = rmap;
+    if (zl < 0 && nbr_src(f.zlo, a, map, rmap, s, m, r)) {
+        ws = s * nc + comp;
         zs = z + a.nzv;
-    } else if (zl >= a.nzv && f.zhi >= 0) {
-        ws = f.zhi * nc + comp;
+        zm = m;
+        zr = r;
+    } else if (zl >= a.nzv && nbr_src(f.zhi, a, map, rmap, s, m, r)) {
+        ws = s * nc + comp;
         zs = z - a.nzv;
+        zm = m;
+        zr = r;
     }
     const bool centre = zl >= 0 && zl < a.nzv;  // halo planes: only their column rows are used
     mbar_arrive_expect_tx(bar, tx_bytes);
     const int bx = a.box_x;
-    tma_load_plane(stage + bx, map, bar, c.x0, c.y0, zs, ws);
-    if (centre && f.top && f.ylo >= 0)
-        tma_load_plane(stage, rmap, bar, c.x0, c.y0 - 1 + a.nyv, zs, f.ylo * nc + comp);
+    tma_load_plane(stage + bx, zm, bar, c.x0, c.y0, zs, ws);
+    if (centre && f.top && nbr_src(f.ylo, a, map, rmap, s, m, r))
+        tma_load_plane(stage, r, bar, c.x0, c.y0 - 1 + a.nyv, zs, s * nc + comp);
     else
-        tma_load_plane(stage, rmap, bar, c.x0, c.y0 - 1, zs, ws);
-    if (centre && f.bot && f.yhi >= 0)
-        tma_load_plane(stage + (c.ny + 1) * bx, rmap, bar, c.x0, c.y0 + c.ny - a.nyv, zs, f.yhi * nc + comp);
+        tma_load_plane(stage, zr, bar, c.x0, c.y0 - 1, zs, ws);
+    if (centre && f.bot && nbr_src(f.yhi, a, map, rmap, s, m, r))
+        tma_load_plane(stage + (c.ny + 1) * bx, r, bar, c.x0, c.y0 + c.ny - a.nyv, zs, s * nc + comp);
     else
-        tma_load_plane(stage + (c.ny + 1) * bx, rmap, bar, c.x0, c.y0 + c.ny, zs, ws);
+        tma_load_plane(stage + (c.ny + 1) * bx, zr, bar, c.x0, c.y0 + c.ny, zs, ws);
     tma_load_plane(stage + a.xh_off, xmap, bar, c.y0 - g, 0, z - g, w);
 }
 
@@ -1032,6 +1061,7 @@ int tm_march_plan_destroy(tm_march_plan *p) {
     cudaFree(p->d_cols);
     cudaFree(p->d_segs);
     cudaFree(p->d_seg_begin);
+    cudaFree(p->d_peer_maps);
     delete p;
     return TM_OK;
 }
@@ -1050,7 +1080,7 @@ namespace {
 int heat_march_impl(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew, int32_t ncomp_sweep,
                     double dxi0, double dxi1, double dxi2, double dtD, int32_t halo_mode, const double *xh_old,
                     double *xh_new, const int32_t *d_nbr, int32_t reverse, const int64_t *fill_cells, int64_t nfill,
-                    void *stream) {
+                    void *stream, int32_t peer_set = -1) {
     using namespace tmk;
     if (!p) return fail(TM_ERR_INVALID, "tm_heat_march: null plan");
     int rc = check_layout(layout, "tm_heat_march");
@@ -1125,6 +1155,16 @@ int heat_march_impl(tm_march_plan *p, const tm_layout *layout, const double *uol
     a.xh_new = xh_new;
     a.nbr = d_nbr;
     a.gw = const_cast<double *>(uold);  // TM_HALO_FUSED_NBR_GHOSTS only: uold's face ghosts (documented)
+    if (peer_set >= 0) {
+        if (halo_mode != TM_HALO_FUSED_NBR)
+            return fail(TM_ERR_INVALID, "tm_heat_march_peer: peer faces ride on TM_HALO_FUSED_NBR");
+        if (peer_set >= TM_PEER_SETS || p->peer_n[peer_set] < 0)
+            return fail(TM_ERR_INVALID, "tm_heat_march_peer: peer set " + std::to_string(peer_set) +
+                                            " not encoded (tm_march_plan_set_peers)");
+        if (p->peer_box_x != a.box_x || p->peer_box_y != p->max_ny)
+            return fail(TM_ERR_INVALID, "tm_heat_march_peer: peer maps encoded for another column box");
+        a.pmaps = p->d_peer_maps + (size_t)peer_set * TM_MAX_PEERS * 2;
+    }
     const size_t smem = (size_t)kHeatStages * stage * sizeof(double) + 2 * kHeatStages * sizeof(uint64_t);
     if (smem > 220 * 1024) return fail(TM_ERR_INVALID, "tm_heat_march: column plane too large for shared memory");
     CUtensorMap map, xmap;
@@ -1186,6 +1226,58 @@ int tm_heat_march(tm_march_plan *p, const tm_layout *layout, const double *uold,
                   double *xh_new, const int32_t *d_nbr, int32_t reverse, void *stream) {
     return heat_march_impl(p, layout, uold, unew, ncomp_sweep, dxi0, dxi1, dxi2, dtD, halo_mode, xh_old, xh_new,
                            d_nbr, reverse, nullptr, 0, stream);
+}
+
+int tm_march_plan_set_peers(tm_march_plan *p, int32_t set, const tm_layout *layout, int32_t npeers,
+                            const double *const *peer_base, const int64_t *peer_nslots) {
+    using namespace tmk;
+    if (!p) return fail(TM_ERR_INVALID, "tm_march_plan_set_peers: null plan");
+    int rc = check_layout(layout, "tm_march_plan_set_peers");
+    if (rc) return rc;
+    if (set < 0 || set >= TM_PEER_SETS) return fail(TM_ERR_INVALID, "tm_march_plan_set_peers: bad set");
+    if (npeers < 0 || npeers > TM_MAX_PEERS || (npeers && (!peer_base || !peer_nslots)))
+        return fail(TM_ERR_INVALID, "tm_march_plan_set_peers: 0..TM_MAX_PEERS peers with bases and slot counts");
+    if (p->ncols && !(p->uniform_ny && p->max_nx % 16 == 0))
+        return fail(TM_ERR_INVALID, "tm_march_plan_set_peers: peer faces need the neighbour-halo march "
+                                    "(columns of one height, width a multiple of 16)");
+    if (!p->d_peer_maps) {
+        cudaError_t e = cudaMalloc(&p->d_peer_maps, sizeof(CUtensorMap) * TM_PEER_SETS * TM_MAX_PEERS * 2);
+        if (e != cudaSuccess) return cuda_fail(e, "tm_march_plan_set_peers: cudaMalloc");
+    }
+    // the column box of the fused (packed) march: max_nx x max_ny rows, and a one-row box
+    const int bx = p->max_nx, by = p->max_ny;
+    CUtensorMap maps[TM_MAX_PEERS * 2];
+    memset(maps, 0, sizeof(maps));
+    for (int i = 0; i < npeers; ++i) {
+        if (!peer_base[i] || peer_nslots[i] < 1)
+            return fail(TM_ERR_INVALID, "tm_march_plan_set_peers: peer " + std::to_string(i) + " has no storage");
+        tm_layout P = *layout;
+        P.nslots = peer_nslots[i];
+        if (p->ncols) {
+            rc = encode_plane_map(&maps[2 * i], P, peer_base[i], bx, by);
+            if (rc) return rc;
+            rc = encode_plane_map(&maps[2 * i + 1], P, peer_base[i], bx, 1);
+            if (rc) return rc;
+        }
+    }
+    // synchronous upload: setup time, outside any capture; queued launches of this plan may
+    // still read the set's previous maps, so drain first
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) return cuda_fail(e, "tm_march_plan_set_peers: synchronize");
+    e = cudaMemcpy(p->d_peer_maps + (size_t)set * TM_MAX_PEERS * 2, maps, sizeof(maps), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "tm_march_plan_set_peers: cudaMemcpy");
+    p->peer_n[set] = npeers;
+    p->peer_box_x = bx;
+    p->peer_box_y = by;
+    return TM_OK;
+}
+
+int tm_heat_march_peer(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,
+                       int32_t ncomp_sweep, double dxi0, double dxi1, double dxi2, double dtD, const double *xh_old,
+                       double *xh_new, const int32_t *d_nbr, int32_t set, int32_t reverse, void *stream) {
+    if (set < 0) return tmk::fail(TM_ERR_INVALID, "tm_heat_march_peer: bad peer set");
+    return heat_march_impl(p, layout, uold, unew, ncomp_sweep, dxi0, dxi1, dxi2, dtD, TM_HALO_FUSED_NBR, xh_old,
+                           xh_new, d_nbr, reverse, nullptr, 0, stream, set);
 }
 
 int tm_heat_march_fill(tm_march_plan *p, const tm_layout *layout, const double *uold, double *unew,

@@ -28,4 +28,9 @@ struct tm_march_plan {
     int32_t x0_common = -1;  // the x0 every column starts at, or -1
     int32_t last_halo_mode = -1;          // mode of the last fused tm_heat_march (tm_march_plan_reset_halos)
     const void *last_xh_new = nullptr;    // and the packed x halo it wrote
+    // peer sets (tm_march_plan_set_peers): per set, 2 TMA maps per peer (column rows, one row)
+    // over another rank's storage, in device memory; -1 = set not encoded
+    CUtensorMap *d_peer_maps = nullptr;  // [TM_PEER_SETS][TM_MAX_PEERS][2]
+    int32_t peer_n[TM_PEER_SETS] = {-1, -1, -1, -1};
+    int32_t peer_box_x = 0, peer_box_y = 0;  // the column box the maps were encoded for
 };

@@ -19,6 +19,10 @@ Two step implementations, bit-identical in the valid cells:
   regular FillBoundary at the end of ``advance``, so the MultiFab handed
   back has every ghost filled.
 
+Multi-rank, ``exchange="peer"``: the march reads the faces of boxes on other
+ranks straight from their storage over NVLink (``peer.PeerFused``), one
+device barrier launch between steps; no pack, message or unpack.
+
 Multi-rank: fused, the march scatters into local neighbours and the faces
 shared with other ranks travel as one packed all-to-all (NCCL) of the new
 field right after it; unfused, the interior tiles are swept while the halo
@@ -47,7 +51,7 @@ class HeatRunner:
 
     def __init__(self, mf: MultiFab, geom: Geometry, params: HeatParams, schedule=None,
                  plan: FillPlan | None = None, use_graph: bool | None = None, zmerge: bool = False,
-                 fused: bool | None = None, march_rows: int | None = None):
+                 fused: bool | None = None, march_rows: int | None = None, exchange: str = "nccl"):
         from . import march
 
         self.geom = geom
@@ -67,7 +71,21 @@ class HeatRunner:
         if fused and not can_fuse:
             raise ValueError("fused halo path needs a uniform fully-covered box layout")
         self.fused = can_fuse if fused is None else fused
-        self.fh = march.FusedHalo(self.a, self.b, geom, march_rows, fill_plan=self.plan) if self.fused else None
+        if exchange not in ("nccl", "peer"):
+            raise ValueError(f"exchange must be 'nccl' or 'peer', not {exchange!r}")
+        self.exchange = exchange if (self.fused and world > 1) else "nccl"
+        if self.exchange == "peer":
+            # faces on other ranks read over NVLink by the march itself (peer.py); ranks that
+            # share a GPU are ordered by the host instead of the device barrier
+            from .peer import PeerFused, ranks_share_device
+
+            shared = ranks_share_device(mf.device)
+            self.fh = PeerFused.connect(self.a, self.b, geom, barrier="host" if shared else "device",
+                                        max_rows=march_rows)
+            if shared:
+                self.use_graph = False
+        else:
+            self.fh = march.FusedHalo(self.a, self.b, geom, march_rows, fill_plan=self.plan) if self.fused else None
         self._graph = None
         self._long = None  # one-rank: LONG_PAIRS captured pairs per replay (see advance)
         self._graph_pairs = 2 if (not self.fused and world == 1) else 1
@@ -83,6 +101,8 @@ class HeatRunner:
         if self.fused:
             # multi-rank: march (boundary and interior columns as two launches when both
             # exist), pack, unpack (+ x-halo refresh when an x face is remote)
+            if self.exchange == "peer":
+                return 1 + (self.fh.barrier is not None)  # march + device barrier
             if self.fh.remote:
                 return 3 + (self.fh._remote_x is not None) + (self.fh.comm is not None)
             return 1
