@@ -45,14 +45,18 @@ __device__ __forceinline__ uint64_t globaltimer() {
     return t;
 }
 
-// One warp; lane i < npeers serves peer i.  The preceding kernels on the stream have
-// completed (no programmatic overlap with this launch), so their writes are ordered
-// before the release; the acquire orders the peers' writes before the kernels after us.
+// One warp; lane i < npeers serves peer i.  Launched with programmatic stream serialization
+// (its launch overlaps the march before it): griddepcontrol.wait returns once that march has
+// completed with its writes visible, the system-scope release publishes them to the peers,
+// the acquire orders the peers' writes before the kernels after us (the next march waits for
+// this grid to complete).
 __global__ void peer_barrier_kernel(uint64_t *inbox, uint64_t *const *peer_inbox, const int32_t *peer_ranks,
                                     int32_t npeers, int32_t my_rank, uint64_t *epoch, int32_t *status,
                                     int64_t timeout_ns) {
     __shared__ uint64_t target;
     const int lane = threadIdx.x;
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the next march's prologue may start
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (lane == 0) {
         target = *epoch + 1;
         *epoch = target;
@@ -60,7 +64,8 @@ __global__ void peer_barrier_kernel(uint64_t *inbox, uint64_t *const *peer_inbox
     __syncwarp();
     const uint64_t e = target;
     if (lane < npeers) {
-        __threadfence_system();
+        // the release is the only system-scope fence (an extra fence.acq_rel.sys costs ~1.3 us:
+        // tools/micro/barrier_probe.cu)
         red_release_sys(peer_inbox[lane] + my_rank, 1ull);
         const uint64_t *mine = inbox + peer_ranks[lane];
         const uint64_t t0 = globaltimer();
@@ -125,9 +130,18 @@ int tm_peer_barrier(uint64_t *inbox, uint64_t *const *peer_inbox, const int32_t 
     if (!inbox || !epoch || !status || (npeers && (!peer_inbox || !peer_ranks)))
         return fail(TM_ERR_INVALID, "tm_peer_barrier: null argument");
     if (timeout_ns <= 0) return fail(TM_ERR_INVALID, "tm_peer_barrier: timeout must be positive");
-    peer_barrier_kernel<<<1, 32, 0, as_stream(stream)>>>(inbox, peer_inbox, peer_ranks, npeers, my_rank, epoch,
-                                                         status, timeout_ns);
-    cudaError_t e = cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(32);
+    cfg.stream = as_stream(stream);
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, peer_barrier_kernel, inbox, peer_inbox, peer_ranks, npeers, my_rank,
+                                       epoch, status, timeout_ns);
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_fail(e, "tm_peer_barrier launch");
     return TM_OK;
 }
