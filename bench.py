@@ -564,7 +564,9 @@ def make_runner(args, HeatRunner, mf, geom, params, sched, plan, world, dev):
     try:
         peer_face_table(mf, geom)
         n = torch.cuda.device_count()
-        if not all(torch.cuda.can_device_access_peer(dev.index, j) for j in range(n) if j != dev.index):
+        if os.environ.get("TM_DIST_BACKEND", "nccl") == "nccl" and n < world:
+            ok, why = 0, f"{n} visible GPUs < {world} ranks: peers' memory cannot be mapped"
+        elif not all(torch.cuda.can_device_access_peer(dev.index, j) for j in range(n) if j != dev.index):
             ok, why = 0, "no peer access between the GPUs"
     except ValueError as e:
         ok, why = 0, str(e)
@@ -585,8 +587,20 @@ def make_runner(args, HeatRunner, mf, geom, params, sched, plan, world, dev):
     del ref, ref_mf
     probe_mf = mf.clone_empty()
     probe_mf.data.copy_(mf.data)
-    probe = HeatRunner(probe_mf, geom, params, sched, plan, exchange="peer", use_graph=False)
+    try:  # IPC mapping can fail (e.g. a device not visible); every collective of the setup is done by then
+        probe = HeatRunner(probe_mf, geom, params, sched, plan, exchange="peer", use_graph=False)
+        ok, why = 1, "ok"
+    except Exception as e:  # noqa: BLE001 -- any setup failure means: use NCCL
+        probe, ok, why = None, 0, f"peer setup failed: {e}"[:200]
+    flag = torch.tensor([ok], dtype=torch.int32, device=dev)
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+    if int(flag.item()) != 1:
+        if probe is not None:
+            probe.fh.close()
+        return HeatRunner(mf, geom, params, sched, plan, **kw), {"used": False, "why": why}
     same = torch.equal(probe.advance(4).data.view(torch.int64), want.view(torch.int64))
+    if probe.fh.barrier is not None and probe.fh.barrier.timed_out():
+        same = False
     torch.cuda.synchronize()
     dist.barrier()
     probe.fh.close()
