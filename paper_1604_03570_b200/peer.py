@@ -192,27 +192,29 @@ class PeerFused:
         every: list = [None] * dist.get_world_size(group)
         dist.all_gather_object(every, mine, group=group)
         _, peers = peer_face_table(a, geom)
-        opened, fields = [], {}
+        # one mapping per exported allocation: a peer's fields (and inbox) may share one
+        # caching-allocator segment, i.e. one IPC handle at different offsets
+        bases: dict = {}
+
+        def open_(h):
+            handle, off = h
+            if handle not in bases:
+                bases[handle] = ipc_open(handle, 0)
+            return bases[handle] + off
+
+        fields = {}
         for r in peers:
             e = every[r]
             if e["layout"] != mine["layout"]:
                 raise ValueError(f"peer halos: rank {r} has another storage layout")
-            pa = ipc_open(*e["a"])
-            pb = ipc_open(*e["b"])
-            opened += [(pa, e["a"][1]), (pb, e["b"][1])]
-            fields[r] = (pa, pb)
+            fields[r] = (open_(e["a"]), open_(e["b"]))
         self = cls(a, b, geom, fields, max_rows, nctas)
         if bar is not None:
-            inbox = []
-            for r in self.peers:
-                p = ipc_open(*every[r]["inbox"])
-                opened.append((p, every[r]["inbox"][1]))
-                inbox.append(p)
-            bar.bind(self.peers, inbox)
+            bar.bind(self.peers, [open_(every[r]["inbox"]) for r in self.peers])
             self.barrier = bar
         else:
             self.host_barrier, self.host_group = True, group
-        self._opened = opened
+        self._opened = [(p, 0) for p in bases.values()]
         return self
 
     def close(self) -> None:

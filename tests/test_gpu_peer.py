@@ -137,7 +137,7 @@ def free_port():
         return s.getsockname()[1]
 
 
-def worker(rank, world, port, out, n, mgs):
+def worker(rank, world, port, out, n, mgs, ncomp=1, nghost=1):
     import torch.distributed as dist
 
     import paper_1604_03570_b200 as tm
@@ -149,8 +149,8 @@ def worker(rank, world, port, out, n, mgs):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         steps = 7
-        geom, ba, glob = _problem(n, mgs, 1, 1, steps)
-        mf = tm.MultiFab(ba, 1, 1)
+        geom, ba, glob = _problem(n, mgs, ncomp, nghost, steps)
+        mf = tm.MultiFab(ba, ncomp, nghost)
         mf.from_global(glob)
         p = tm.HeatParams.stable(1.0, geom.dx)
         r = HeatRunner(mf, geom, p, fused=True, exchange="peer")
@@ -164,10 +164,10 @@ def worker(rank, world, port, out, n, mgs):
             v = ba[u]
             sl = (slice(None),) + tuple(slice(v.lo[d], v.hi[d] + 1) for d in (2, 1, 0))
             mine[sl] = ref[sl]
-        h = orc.HostMF(list(ba), 1, 1)
+        h = orc.HostMF(list(ba), ncomp, nghost)
         h.from_global(ref)
-        # finalize ran a FillBoundary (NCCL path over gloo): ghosts too must be right
-        out[rank] = (bool(np.array_equal(got, mine)), fin.reduce_sum(0) == orc.reduce_sum(h, 0))
+        out[rank] = (bool(np.array_equal(got, mine)),
+                     all(fin.reduce_sum(k) == orc.reduce_sum(h, k) for k in range(ncomp)))
         torch.cuda.synchronize()
         dist.barrier()
         r.fh.close()
@@ -175,11 +175,14 @@ def worker(rank, world, port, out, n, mgs):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,mgs,world", [(64, 32, 2), (128, 32, 2)])
-def test_two_processes_ipc_match_oracle(n, mgs, world):
+@pytest.mark.parametrize("n,mgs,world,ncomp,nghost", [(64, 32, 2, 1, 1), (128, 32, 2, 1, 1), (64, 32, 2, 2, 2),
+                                                       (128, 32, 4, 1, 1)])
+def test_two_processes_ipc_match_oracle(n, mgs, world, ncomp, nghost):
+    """Real CUDA IPC between processes sharing cuda:0 (2 ranks; 4 ranks: every box has remote
+    z faces on two different peers)."""
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(worker, args=(world, free_port(), out, n, mgs), nprocs=world, join=True)
+    mp.spawn(worker, args=(world, free_port(), out, n, mgs, ncomp, nghost), nprocs=world, join=True)
     for r in range(world):
         ok, sum_ok = out[r]
         assert ok, f"rank {r}: boxes differ from the oracle"
