@@ -200,30 +200,101 @@ def cpu_reference_rate(w, budget_s: float, steps: int | None = None, boxes: int 
     return rate, threads, sample, n, nb, el
 
 
+REF_INSTALL = os.path.join(os.path.dirname(os.path.abspath(__file__)), "baseline", "_ref")
+
+
+def numba_reference_rate(w, threads: int, steps: int | None, budget_s: float, warmup: int = 1):
+    """The UNMODIFIED reference (pip-installed into baseline/_ref by __graft_entry__.build())
+    through its own public API and timing loop shape (tilemesh/bench.py:183-206: fill_boundary
+    + heat_step per step, JIT warmed outside the timed region) on workload ``w`` with all
+    boxes.  Returns None when the install or numba is absent on this host.  ``steps`` is
+    capped so the timed loop stays within ``budget_s`` seconds."""
+    if not os.path.isdir(os.path.join(REF_INSTALL, "tilemesh")):
+        return None
+    sys.path.insert(0, REF_INSTALL)
+    try:
+        from tilemesh.bench import RunConfig, _setup, _steppers
+        from tilemesh.level import build_fill_plan, fill_boundary
+    except Exception:  # numba / matplotlib missing on this host
+        return None
+    finally:
+        sys.path.remove(REF_INSTALL)
+    if w.ncomp != 1 or w.nghost != 1:
+        return None  # the reference's bench set-up is one component, one ghost layer
+    e = w.domain.extents
+    cfg = RunConfig(nx=e[0], ny=e[1], nz=e[2], max_grid_size=w.max_grid_size, tile_size=tuple(w.tile_size),
+                    threads=threads, steps=0)
+    geom, old = _setup(cfg)  # the reference's own cosine init: values change no code path
+    new = old.clone_empty()
+    plan = build_fill_plan(old, geom)
+    step, _ = _steppers(cfg, geom, old)
+    t0 = time.perf_counter()
+    for _ in range(max(1, warmup)):  # JIT + page-in
+        fill_boundary(old, geom, plan, threads)
+        step(old, new)
+        old, new = new, old
+    t0 = time.perf_counter()
+    fill_boundary(old, geom, plan, threads)
+    step(old, new)
+    old, new = new, old
+    per = time.perf_counter() - t0
+    cap = max(1, int(budget_s / max(per, 1e-9)))
+    n = cap if steps is None else max(1, min(steps, cap))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        fill_boundary(old, geom, plan, threads)
+        step(old, new)
+        old, new = new, old
+    el = time.perf_counter() - t0
+    rate = w.cells * n / el
+    sample = (f"{w.name}: all {len(old.units)} boxes, {n} x (fill_boundary + heat_step) of the unmodified reference "
+              f"(tilemesh 0.1.0, numba, baseline/_ref), threads={threads}, {el:.2f} s")
+    return rate, threads, sample, n, el
+
+
 def run_reference(args, w):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    import paper_1604_03570_b200 as tm
+
+    nboxes = len(tm.BoxArray.chop(w.domain, w.max_grid_size))
     # bound each step: size the per-step sample so the whole run is ~a minute
     total = max(args.steps + args.warmup, 1)
     per_step_budget = 60.0 / total
     probe_rate, _, _, _, _, _ = cpu_reference_rate(w, budget_s=1.0, steps=1, boxes=1)
-    box_cells = w.cells // len(__import__("paper_1604_03570_b200").BoxArray.chop(w.domain, w.max_grid_size))
+    box_cells = w.cells // nboxes
     boxes = max(1, int(per_step_budget * probe_rate / box_cells))
     if args.warmup:
         cpu_reference_rate(w, 0, steps=args.warmup, boxes=boxes)
     rate, cores, sample, n, nb, el = cpu_reference_rate(w, 0, steps=args.steps, boxes=boxes)
+    port = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
+            "ms_per_step": el / n * 1e3, "sample_boxes_per_step": nb}
+    # the unmodified reference itself, when its install travelled to this host (all boxes per
+    # step; steps capped to ~60 s of timed work)
+    threads = len(os.sched_getaffinity(0))
+    ref = None
+    try:
+        ref = numba_reference_rate(w, threads, args.steps, 60.0, warmup=max(1, min(args.warmup, 3)))
+    except Exception as exc:  # never lose the arm to the optional leg
+        port["reference_error"] = f"{type(exc).__name__}: {exc}"[:200]
+    if ref is not None:
+        r_rate, r_cores, r_sample, r_n, r_el = ref
+        value, ms, cpu = r_rate, r_el / r_n * 1e3, {"value": r_rate, "unit": UNIT, "cores": r_cores,
+                                                    "kind": "reference", "sample": r_sample, "steps_timed": r_n,
+                                                    "port": port}
+    else:
+        value, ms, cpu = rate, el / n * 1e3, port
     line = {
-        "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": el / n * 1e3, "higher_is_better": True, "scaling": args.scaling,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{w.name}: periodic {w.domain.extents[0]}x{w.domain.extents[1]}x"
                                f"{w.domain.extents[2]}, max_grid_size {w.max_grid_size} "
-                               f"({len(__import__('paper_1604_03570_b200').BoxArray.chop(w.domain, w.max_grid_size))} "
-                               f"boxes), nghost {w.nghost}, ncomp {w.ncomp}, tile {w.tile_size}",
-                   "sample_boxes_per_step": nb},
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
-        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                               f"({nboxes} boxes), nghost {w.nghost}, ncomp {w.ncomp}, tile {w.tile_size}",
+                   "sample_boxes_per_step": nboxes if ref is not None else nb},
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
@@ -482,6 +553,13 @@ def run_ours(args, w):
             rate1, _, sample1, _, _, _ = cpu_reference_rate(w, args.cpu_seconds / 2, threads=1)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample,
                    "one_core": {"value": rate1, "cores": 1, "sample": sample1}}
+            try:  # the unmodified reference beside the port, when its install is on this host
+                ref = numba_reference_rate(w, cores, None, args.cpu_seconds)
+                if ref is not None:
+                    cpu["unmodified_reference"] = {"value": ref[0], "unit": UNIT, "cores": ref[1],
+                                                   "kind": "reference", "sample": ref[2]}
+            except Exception as exc:
+                cpu["unmodified_reference"] = {"error": f"{type(exc).__name__}: {exc}"[:200]}
         traffic = profile_traffic(w.name, runner.fused)
         others = config_records(args, peak) if world == 1 and args.configs else None
         launches_per_step = runner.launches_per_step
