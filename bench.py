@@ -395,10 +395,6 @@ def run_ours(args, w):
     ev_mid = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        # the same call as the timed one, untimed: a short advance replays ONE chain captured for
-        # its length (HeatRunner._chain), and the capture must not happen inside the timed region
-        for _ in range(1 + args.steps % 2):  # twice when K is odd: the timed call starts on an even step
-            runner.advance(args.steps, finalize=False)
         runner.advance(args.hot_steps + (args.hot_steps % 2), finalize=False)
         barrier()
         torch.cuda._sleep(400_000)  # ~0.2 ms at 1.965 GHz

@@ -48,7 +48,6 @@ class HeatRunner:
     """Owns the old/new pair and advances it ``n`` steps at a time."""
 
     LONG_PAIRS = 8  # captured pairs per replay of the long graph (one rank)
-    CHAIN_MAX = 32  # advances of up to this many pair units replay one chain captured for that length
 
     def __init__(self, mf: MultiFab, geom: Geometry, params: HeatParams, schedule=None,
                  plan: FillPlan | None = None, use_graph: bool | None = None, zmerge: bool = False,
@@ -89,7 +88,6 @@ class HeatRunner:
             self.fh = march.FusedHalo(self.a, self.b, geom, march_rows, fill_plan=self.plan) if self.fused else None
         self._graph = None
         self._long = None  # one-rank: LONG_PAIRS captured pairs per replay (see advance)
-        self._chains = {}  # one-rank: chains captured for exactly one short advance's length
         self._graph_pairs = 2 if (not self.fused and world == 1) else 1
         self._primed = False
         self.steps_done = 0
@@ -126,7 +124,6 @@ class HeatRunner:
             torch.cuda.synchronize()
             self._graph = None
             self._long = None
-            self._chains = {}
 
     def _step(self, old: MultiFab, new: MultiFab) -> None:
         if self.fused:  # b -> a steps walk backwards: they start where a -> b ended (L2)
@@ -174,29 +171,6 @@ class HeatRunner:
             torch.cuda.current_stream().wait_stream(s)
             self._long = gl
 
-    def _chain(self, units: int):
-        """A graph of ``units`` captured pair units (cached, a handful of lengths)."""
-        import torch
-
-        from .multifab import snapshots_in_capture
-
-        g = self._chains.get(units)
-        if g is None:
-            if len(self._chains) >= 4:
-                self._chains.pop(next(iter(self._chains)))
-            torch.cuda.synchronize()
-            g = torch.cuda.CUDAGraph()
-            s = torch.cuda.Stream()
-            s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s), snapshots_in_capture():
-                with torch.cuda.graph(g, stream=s):
-                    for _ in range(units * self._graph_pairs):
-                        self._step(self.a, self.b)
-                        self._step(self.b, self.a)
-            torch.cuda.current_stream().wait_stream(s)
-            self._chains[units] = g
-        return g
-
     def _verify_capture(self) -> None:
         """Multi-rank: replay the captured pair once and redo the same two
         steps eagerly from the same state; keep the graph only if every rank
@@ -240,16 +214,6 @@ class HeatRunner:
                 self._capture()
                 self.steps_done += need
                 k += need
-            unit = 2 * self._graph_pairs
-            if (self.steps_done % 2 == 0 and self._long is not None
-                    and self.LONG_PAIRS < (n - k) // unit <= self.CHAIN_MAX and (n - k) // unit != 2 * self.LONG_PAIRS):
-                # a short advance (the driver's bench: 20 steps) as ONE replay of a chain captured
-                # for exactly that length: every graph boundary inside it costs a launch gap and
-                # the PDL overlap of two steps
-                m = (n - k) // unit
-                self._chain(m).replay()
-                self.steps_done += m * unit
-                k += m * unit
             if self.steps_done % 2 == 0 and self._long is not None:
                 while n - k >= 2 * self._graph_pairs * self.LONG_PAIRS:
                     self._long.replay()
