@@ -196,3 +196,41 @@ def test_wide4_stays_inside_its_allocations(tm, n, mgs, fused):
         assert g.check() == []
     want = orc.wide4_periodic(glob[0], steps, coeffs.as_array(), (1.0 / w.dx ** 2,) * 3, dt)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,mgs,ranks,ncomp,nghost", [(128, 32, 8, 1, 1), (64, 32, 2, 2, 2)])
+def test_peer_march_stays_inside_every_ranks_allocations(tm, n, mgs, ranks, ncomp, nghost):
+    """Peer halos with emulated ranks on one GPU (tests/test_gpu_peer.py): every
+    rank's fields, halo buffers and peer tables are guarded, so a march that
+    reads a peer's face must not write outside its own rank's storage either."""
+    import torch
+
+    from paper_1604_03570_b200.boxarray import DistributionMapping
+    from paper_1604_03570_b200.peer import PeerFused
+
+    steps = 4
+    w = tm.CONFIGS["C5"].scaled(n, mgs, steps)
+    geom = tm.Geometry(w.domain, (True, True, True), (w.dx,) * 3)
+    ba = tm.BoxArray.chop(w.domain, mgs)
+    glob = np.random.default_rng(11).standard_normal((ncomp,) + tuple(w.domain.extents[::-1]))
+    dm = DistributionMapping(ba, ranks)
+    p = tm.HeatParams.stable(1.0, geom.dx)
+    with GuardBands() as g:
+        pairs = []
+        for r in range(ranks):
+            a = tm.MultiFab(ba, ncomp, nghost, dm=dm, rank=r)
+            a.from_global(glob)
+            pairs.append((a, a.clone_empty()))
+        fields = {r: (pr[0].ptr, pr[1].ptr) for r, pr in enumerate(pairs)}
+        pfs = [PeerFused(a, b, geom, fields) for a, b in pairs]
+        for (a, _), pf in zip(pairs, pfs):
+            pf.prime(a)
+        for k in range(steps):
+            for (a, b), pf in zip(pairs, pfs):
+                old, new = (a, b) if k % 2 == 0 else (b, a)
+                pf.step(new, old, p, reverse=k % 2 == 1)
+        torch.cuda.synchronize()
+        got = sum(pr[steps % 2].to_global().cpu().numpy() for pr in pairs)
+        assert g.check() == []
+    c = p.coefficients()
+    assert np.array_equal(got, orc.heat_periodic(glob, steps, c[:3], c[3]))
