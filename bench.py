@@ -600,6 +600,12 @@ def run_ours(args, w):
                 "peak_source": peak_src,
                 # north_star quotes "roughly 8 TB/s"; SURVEY.md §8d asks for both figures
                 "frac_vs_nominal_8000_gbs": achieved / 8000.0,
+                # context, static: what a plain copy of one C2 launch's bytes does at this size
+                **({"same_size_copy_note":
+                     "a plain copy of 134 MB read + 134 MB written in one launch (296 CTAs) takes ~46.1 us with "
+                     "equal static shares (0.89 of the peak) and 43.4 us with dynamic shares (0.94): "
+                     "tools/micro/sm_rate.cu, profiles/r02/sm_rate_copy_probe.txt"}
+                   if w.name == "C2" and world == 1 else {}),
             },
             "unfused_components": {"fill_boundary_ms": fill_ms, "fill_ghost_gbs": fill_gbs,
                                    "ghost_cells": ghost_cells, "heat_step_ms": sweep_ms,
